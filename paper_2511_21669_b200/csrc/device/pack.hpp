@@ -1,0 +1,28 @@
+// pack.hpp — host-side batch packing shared by the CUDA runtime.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "dsdsim.h"
+#include "layout.cuh"
+#include "runtime.hpp"
+
+namespace dsd {
+
+struct Packed {
+    std::vector<char> blob;
+    std::vector<DevScenario> scen;
+    Caps caps{};
+    std::vector<uint32_t> rep_scen;
+    std::vector<uint64_t> seed, gseed;
+};
+
+// Validates the scenarios (reference error texts, DSD_ERR_CONFIG) and packs
+// them into the scenario blob; computes the batch capacities.
+Packed pack_batch(const dsd_scenario* scenarios, size_t n_scenarios, const dsd_replica* replicas, size_t n);
+
+// Assigns the workspace field pointers inside [base, base + bytes) and
+// returns bytes; with base == nullptr it only sizes.
+size_t layout_workspace(Workspace& W, const Caps& c, char* base);
+
+}  // namespace dsd

@@ -1,0 +1,300 @@
+// capi.cpp — extern "C" boundary (include/dsdsim.h).  Every entry point
+// converts dsd::Error / std::exception into a status code + message, so no
+// exception crosses the ABI.
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../device/runtime.hpp"
+#include "dsdsim.h"
+#include "report.hpp"
+#include "resolve.hpp"
+#include "sweep.hpp"
+
+struct dsd_handle {
+    std::unique_ptr<dsd::Runtime> rt;
+    dsd::host::Caches caches;
+    std::unique_ptr<dsd::host::SweepBatch> prepared_sweep;
+};
+
+namespace {
+
+void put_err(char* err, size_t errlen, const std::string& m) {
+    if (!err || errlen == 0) return;
+    size_t k = std::min(errlen - 1, m.size());
+    std::memcpy(err, m.data(), k);
+    err[k] = '\0';
+}
+
+template <typename F>
+int guard(char* err, size_t errlen, F&& f) {
+    try {
+        f();
+        if (err && errlen) err[0] = '\0';
+        return DSD_OK;
+    } catch (const dsd::Error& e) {
+        put_err(err, errlen, e.what());
+        return e.code;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return DSD_ERR_RUNTIME;
+    }
+}
+
+char* dup(const std::string& s) {
+    char* p = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(p, s.data(), s.size());
+    p[s.size()] = '\0';
+    return p;
+}
+
+void need(dsd_handle* h) {
+    if (!h || !h->rt) throw dsd::Error(DSD_ERR_RUNTIME, "null dsd handle");
+}
+
+}  // namespace
+
+extern "C" {
+
+int dsd_abi_version(void) { return DSD_ABI_VERSION; }
+
+void dsd_free(void* p) { std::free(p); }
+
+int dsd_create(int device_ordinal, dsd_handle** out, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        if (!out) throw dsd::Error(DSD_ERR_RUNTIME, "null output handle");
+        auto h = std::make_unique<dsd_handle>();
+        h->rt = std::make_unique<dsd::Runtime>(device_ordinal);
+        *out = h.release();
+    });
+}
+
+void dsd_destroy(dsd_handle* h) { delete h; }
+
+int dsd_run_batch(dsd_handle* h, const dsd_scenario* scenarios, size_t n_scenarios, const dsd_replica* replicas,
+                  size_t n, const dsd_run_opts* opts, dsd_replica_summary* summaries, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        h->rt->prepare(scenarios, n_scenarios, replicas, n, opts && opts->collect_records);
+        h->rt->launch();
+        h->rt->sync();
+        if (summaries && n) h->rt->summaries(summaries, n);
+    });
+}
+
+int dsd_fetch_records(dsd_handle* h, size_t replica, dsd_request_record* records, size_t records_cap,
+                      int64_t* n_records, int32_t* gamma_seq, int32_t* committed_seq, size_t seq_cap, int64_t* n_seq,
+                      int64_t* busy_us, size_t busy_cap, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        h->rt->fetch_records(replica, records, records_cap, n_records, gamma_seq, committed_seq, seq_cap, n_seq,
+                             busy_us, busy_cap);
+    });
+}
+
+int dsd_batch_prepare(dsd_handle* h, const dsd_scenario* scenarios, size_t n_scenarios, const dsd_replica* replicas,
+                      size_t n, const dsd_run_opts* opts, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        h->rt->prepare(scenarios, n_scenarios, replicas, n, opts && opts->collect_records);
+    });
+}
+
+int dsd_batch_launch(dsd_handle* h, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        h->rt->launch();
+    });
+}
+
+int dsd_batch_sync(dsd_handle* h, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        h->rt->sync();
+    });
+}
+
+int dsd_batch_summaries(dsd_handle* h, dsd_replica_summary* summaries, size_t n, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        h->rt->summaries(summaries, n);
+    });
+}
+
+int dsd_batch_device_summaries(dsd_handle* h, void** dev_ptr, size_t* bytes) {
+    if (!h || !h->rt || !dev_ptr || !bytes) return DSD_ERR_RUNTIME;
+    h->rt->device_summaries(dev_ptr, bytes);
+    return DSD_OK;
+}
+
+void* dsd_stream(dsd_handle* h) { return (h && h->rt) ? h->rt->stream() : nullptr; }
+
+int64_t dsd_last_launch_count(dsd_handle* h) { return (h && h->rt) ? h->rt->last_launch_count() : 0; }
+
+int dsd_last_kernel_ms(dsd_handle* h, double* sim_kernel_ms, double* gen_kernel_ms, double* total_ms) {
+    char err[8];
+    return guard(err, sizeof(err), [&] {
+        need(h);
+        h->rt->last_kernel_ms(sim_kernel_ms, gen_kernel_ms, total_ms);
+    });
+}
+
+int dsd_run_simulation(dsd_handle* h, const char* config_yaml, const char* base_dir, int strict, int has_seed,
+                       uint64_t seed, char** report_json, char** report_csv, uint64_t* events_processed,
+                       int64_t* end_time_us, double* agg, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        dsd::cfg::Node config = dsd::cfg::parse(config_yaml ? config_yaml : "");
+        dsd::host::Resolved rc =
+            dsd::host::resolve_config(config, strict != 0, has_seed ? std::optional<uint64_t>(seed) : std::nullopt,
+                                      base_dir ? base_dir : ".", &h->caches);
+        dsd_replica rep{};
+        rep.scenario = 0;
+        rep.seed = rc.seed;
+        rep.gen_seed = rc.gen_seed;
+        const bool need_records = report_json || report_csv;
+        h->rt->prepare(&rc.scen, 1, &rep, 1, need_records);
+        h->rt->launch();
+        h->rt->sync();
+        dsd::host::ReplicaOutput out;
+        h->rt->summaries(&out.summary, 1);
+        if (out.summary.status != DSD_OK)
+            throw dsd::Error(DSD_ERR_RUNTIME, "engine capacity exceeded on the device (event heap / sequence arena)");
+        if (need_records) {
+            int64_t nrec = 0, nseq = 0;
+            h->rt->fetch_records(0, nullptr, 0, &nrec, nullptr, nullptr, 0, &nseq, nullptr, 0);
+            out.records.resize(static_cast<size_t>(nrec));
+            out.gamma_seq.resize(static_cast<size_t>(nseq));
+            out.committed_seq.resize(static_cast<size_t>(nseq));
+            out.busy_us.resize(static_cast<size_t>(rc.scen.n_targets));
+            h->rt->fetch_records(0, out.records.data(), out.records.size(), &nrec, out.gamma_seq.data(),
+                                 out.committed_seq.data(), out.gamma_seq.size(), &nseq, out.busy_us.data(),
+                                 out.busy_us.size());
+            if (report_json) *report_json = dup(dsd::host::emit_report(out, rc.scen.n_targets, rc.digest, rc.seed));
+            if (report_csv) *report_csv = dup(dsd::host::emit_report_csv(out));
+        }
+        if (events_processed) *events_processed = out.summary.events_processed;
+        if (end_time_us) *end_time_us = out.summary.end_time_us;
+        if (agg) {
+            agg[0] = static_cast<double>(out.summary.completed);
+            agg[1] = out.summary.throughput_rps;
+            agg[2] = out.summary.mean_ttft_ms;
+            agg[3] = out.summary.mean_tpot_ms;
+        }
+    });
+}
+
+int dsd_run_sweep(dsd_handle* h, const char* sweep_yaml, const char* base_dir, const char* out_dir,
+                  char** summary_json, char** summary_csv, double* totals, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        dsd::cfg::Node node = dsd::cfg::parse(sweep_yaml ? sweep_yaml : "");
+        dsd::host::SweepBatch b = dsd::host::plan_sweep(node, base_dir ? base_dir : ".", 0, 1, &h->caches);
+        dsd::host::SweepTotals t = dsd::host::run_sweep(*h->rt, b, out_dir ? out_dir : "");
+        if (summary_json) *summary_json = dup(dsd::host::sweep_summary_json(b.points));
+        if (summary_csv) *summary_csv = dup(dsd::host::sweep_summary_csv(b.points));
+        if (totals) {
+            totals[0] = t.points;
+            totals[1] = t.replicas;
+            totals[2] = t.failed;
+            totals[3] = t.events;
+        }
+    });
+}
+
+int dsd_prepare_sweep(dsd_handle* h, const char* sweep_yaml, const char* base_dir, int shard, int n_shards,
+                      int64_t* n_replicas, int64_t* n_points, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        if (n_shards < 1 || shard < 0 || shard >= n_shards) throw dsd::Error(DSD_ERR_CONFIG, "bad shard index");
+        dsd::cfg::Node node = dsd::cfg::parse(sweep_yaml ? sweep_yaml : "");
+        auto b = std::make_unique<dsd::host::SweepBatch>(
+            dsd::host::plan_sweep(node, base_dir ? base_dir : ".", shard, n_shards, &h->caches));
+        h->rt->prepare(b->scenarios.data(), b->scenarios.size(), b->replicas.data(), b->replicas.size(), false);
+        if (n_replicas) *n_replicas = static_cast<int64_t>(b->replicas.size());
+        if (n_points) *n_points = static_cast<int64_t>(b->points.size());
+        h->prepared_sweep = std::move(b);
+    });
+}
+
+struct dsd_resolved {
+    dsd::host::Resolved rc;
+};
+
+int dsd_resolve_config(const char* config_yaml, const char* base_dir, int strict, int has_seed, uint64_t seed,
+                       dsd_resolved** out, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        dsd::cfg::Node config = dsd::cfg::parse(config_yaml ? config_yaml : "");
+        auto r = std::make_unique<dsd_resolved>();
+        r->rc = dsd::host::resolve_config(config, strict != 0, has_seed ? std::optional<uint64_t>(seed) : std::nullopt,
+                                          base_dir ? base_dir : ".", nullptr);
+        r->rc.bind();
+        *out = r.release();
+    });
+}
+
+const dsd_scenario* dsd_resolved_scenario(const dsd_resolved* r) { return &r->rc.scen; }
+
+void dsd_resolved_replica(const dsd_resolved* r, dsd_replica* out) {
+    *out = dsd_replica{};
+    out->seed = r->rc.seed;
+    out->gen_seed = r->rc.gen_seed;
+}
+
+const char* dsd_resolved_digest(const dsd_resolved* r) { return r->rc.digest.c_str(); }
+
+void dsd_resolved_free(dsd_resolved* r) { delete r; }
+
+struct dsd_sweep_plan {
+    dsd::host::SweepBatch b;
+};
+
+int dsd_plan_sweep(const char* sweep_yaml, const char* base_dir, dsd_sweep_plan** out, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        dsd::cfg::Node node = dsd::cfg::parse(sweep_yaml ? sweep_yaml : "");
+        auto p = std::make_unique<dsd_sweep_plan>();
+        p->b = dsd::host::plan_sweep(node, base_dir ? base_dir : ".", 0, 1, nullptr);
+        for (size_t k = 0; k < p->b.resolved.size(); ++k) {
+            p->b.resolved[k].bind();
+            p->b.scenarios[k] = p->b.resolved[k].scen;
+        }
+        *out = p.release();
+    });
+}
+
+size_t dsd_sweep_plan_scenarios(const dsd_sweep_plan* p, const dsd_scenario** scenarios) {
+    if (scenarios) *scenarios = p->b.scenarios.data();
+    return p->b.scenarios.size();
+}
+
+size_t dsd_sweep_plan_replicas(const dsd_sweep_plan* p, const dsd_replica** replicas) {
+    if (replicas) *replicas = p->b.replicas.data();
+    return p->b.replicas.size();
+}
+
+void dsd_sweep_plan_free(dsd_sweep_plan* p) { delete p; }
+
+int dsd_emit_report(const dsd_replica_summary* summary, const dsd_request_record* records, size_t n_records,
+                    const int32_t* gamma_seq, const int32_t* committed_seq, size_t n_seq, const int64_t* busy_us,
+                    int n_targets, const char* digest, uint64_t seed, char** report_json, char** report_csv) {
+    char err[8];
+    return guard(err, sizeof(err), [&] {
+        dsd::host::ReplicaOutput o;
+        o.summary = *summary;
+        o.records.assign(records, records + n_records);
+        if (n_seq) {
+            o.gamma_seq.assign(gamma_seq, gamma_seq + n_seq);
+            o.committed_seq.assign(committed_seq, committed_seq + n_seq);
+        }
+        o.busy_us.assign(busy_us, busy_us + n_targets);
+        if (report_json) *report_json = dup(dsd::host::emit_report(o, n_targets, digest ? digest : "", seed));
+        if (report_csv) *report_csv = dup(dsd::host::emit_report_csv(o));
+    });
+}
+
+uint64_t dsd_sweep_point_seed(uint64_t base_seed, const char* point_id, int repetition) {
+    return dsd::host::sweep_point_seed(base_seed, point_id ? point_id : "", repetition);
+}
+
+}  // extern "C"

@@ -1,0 +1,262 @@
+// sweep.cpp — run_sweep on the GPU engine (see sweep.hpp).  Point
+// materialisation, seeds, file names and summaries follow
+// proj/src/runner/sweep.cpp:16-199; the per-(point, rep) worker loop
+// (:112-150) becomes one device batch of replicas.
+#include "sweep.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <filesystem>
+#include <fstream>
+#include <thread>
+
+#include "report.hpp"
+
+namespace dsd::host {
+
+using cfg::Node;
+
+SweepSpec SweepSpec::from_node(const Node& node, const std::string& base_dir) {
+    SweepSpec spec;
+    spec.base_dir = base_dir;
+    const Node* base = node.get("base");
+    if (base && base->scalar()) {
+        std::string path = base->to_string();
+        if (!path.empty() && path.front() != '/' && !base_dir.empty() && base_dir != ".") path = base_dir + "/" + path;
+        spec.base = cfg::parse_file(path);
+    } else if (const Node* inl = node.get("config")) {
+        spec.base = *inl;
+    } else {
+        throw Error(DSD_ERR_CONFIG, "sweep spec requires 'base' (path) or 'config' (inline)");
+    }
+    spec.base_seed = static_cast<uint64_t>(node.int_or("seed", 42));
+    spec.repetitions = static_cast<int>(node.int_or("repetitions", 1));
+    if (spec.repetitions < 1) throw Error(DSD_ERR_CONFIG, "sweep repetitions must be >= 1");
+    if (const Node* axes = node.get("axes"); axes && axes->map()) {
+        for (const auto& f : axes->fields) {
+            if (!f.second.seq() || f.second.items.empty())
+                throw Error(DSD_ERR_CONFIG, "sweep axis '" + f.first + "' must be a non-empty list");
+            spec.axes.emplace_back(f.first, f.second.items);
+        }
+    }
+    return spec;
+}
+
+size_t SweepSpec::point_count() const {
+    size_t n = 1;
+    for (const auto& a : axes) n *= a.second.size();
+    return n;
+}
+
+uint64_t sweep_point_seed(uint64_t base_seed, const std::string& point_id, int repetition) {
+    if (point_id == "base" && repetition == 0) return base_seed;
+    return cfg::fnv1a64(point_id + "#rep=" + std::to_string(repetition), base_seed ^ 0x9e3779b97f4a7c15ULL);
+}
+
+namespace {
+
+std::string point_id_of(const std::vector<std::pair<std::string, std::string>>& assignment) {
+    std::vector<std::string> parts;
+    for (const auto& kv : assignment) parts.push_back(kv.first + "=" + kv.second);
+    std::sort(parts.begin(), parts.end());
+    std::string id;
+    for (const auto& p : parts) {
+        if (!id.empty()) id += ';';
+        id += p;
+    }
+    return id.empty() ? "base" : id;
+}
+
+std::string sanitize_filename(const std::string& s) {
+    std::string out;
+    for (char c : s)
+        out += (std::isalnum(static_cast<unsigned char>(c)) || c == '-' || c == '_' || c == '=') ? c : '_';
+    return out.size() > 120 ? out.substr(0, 120) : out;
+}
+
+}  // namespace
+
+SweepBatch plan_sweep(const Node& node, const std::string& base_dir, int shard, int n_shards, Caches* caches) {
+    SweepBatch b;
+    b.spec = SweepSpec::from_node(node, base_dir);
+    const SweepSpec& spec = b.spec;
+    const size_t n_points = spec.point_count();
+    b.points.resize(n_points);
+    for (size_t idx = 0; idx < n_points; ++idx) {
+        size_t rem = idx;
+        auto& asg = b.points[idx].assignment;
+        for (size_t a = spec.axes.size(); a-- > 0;) {
+            const auto& values = spec.axes[a].second;
+            const Node& v = values[rem % values.size()];
+            rem /= values.size();
+            asg.emplace_back(spec.axes[a].first, v.scalar() ? v.to_string() : v.canonical());
+        }
+        std::reverse(asg.begin(), asg.end());
+        b.points[idx].point_id = point_id_of(asg);
+    }
+    // resolve every point once (seed-independent except for the seeds
+    // themselves, which become per-replica parameters)
+    std::vector<Resolved> res(n_points);
+    std::vector<char> ok(n_points, 0);
+    std::atomic<size_t> next{0};
+    auto worker = [&] {
+        for (;;) {
+            size_t idx = next.fetch_add(1);
+            if (idx >= n_points) return;
+            SweepPoint& p = b.points[idx];
+            try {
+                Node config = spec.base;
+                size_t rem = idx;
+                for (size_t a = spec.axes.size(); a-- > 0;) {
+                    const auto& values = spec.axes[a].second;
+                    cfg::set_path(config, spec.axes[a].first, values[rem % values.size()]);
+                    rem /= values.size();
+                }
+                res[idx] = resolve_config(config, true, sweep_point_seed(spec.base_seed, p.point_id, 0),
+                                          spec.base_dir, caches);
+                ok[idx] = 1;
+            } catch (const std::exception& e) {
+                p.failed = true;
+                p.error = e.what();
+            }
+        }
+    };
+    unsigned nthreads = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32u));
+    if (n_points < 64) nthreads = 1;
+    if (nthreads == 1) {
+        worker();
+    } else {
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < nthreads; ++t) pool.emplace_back(worker);
+        for (auto& t : pool) t.join();
+    }
+    b.point_scenario.assign(n_points, -1);
+    for (size_t idx = 0; idx < n_points; ++idx) {
+        if (!ok[idx]) continue;
+        b.point_scenario[idx] = static_cast<int64_t>(b.resolved.size());
+        b.resolved.push_back(std::move(res[idx]));
+    }
+    b.scenarios.reserve(b.resolved.size());
+    for (auto& r : b.resolved) {
+        r.bind();
+        b.scenarios.push_back(r.scen);
+    }
+    int64_t g = 0;
+    for (size_t idx = 0; idx < n_points; ++idx) {
+        const int64_t s = b.point_scenario[idx];
+        if (s < 0) continue;
+        const Resolved& r = b.resolved[static_cast<size_t>(s)];
+        for (int rep = 0; rep < spec.repetitions; ++rep, ++g) {
+            if (n_shards > 1 && g % n_shards != shard) continue;
+            dsd_replica x{};
+            x.scenario = static_cast<uint32_t>(s);
+            x.seed = sweep_point_seed(spec.base_seed, b.points[idx].point_id, rep);
+            x.gen_seed = r.gen_seed_fixed ? r.gen_seed : x.seed;
+            b.replicas.push_back(x);
+            b.replica_origin.emplace_back(static_cast<int64_t>(idx), rep);
+        }
+    }
+    return b;
+}
+
+SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir) {
+    SweepTotals tot;
+    const bool reports = !out_dir.empty();
+    if (reports) std::filesystem::create_directories(out_dir);
+    const size_t n = b.replicas.size();
+    std::vector<dsd_replica_summary> sums(n);
+    if (n > 0) {
+        rt.prepare(b.scenarios.data(), b.scenarios.size(), b.replicas.data(), n, reports);
+        rt.launch();
+        rt.sync();
+        rt.summaries(sums.data(), n);
+    }
+    const int R = b.spec.repetitions;
+    std::vector<double> thr(b.points.size(), 0.0), ttft(b.points.size(), 0.0), tpot(b.points.size(), 0.0);
+    for (size_t k = 0; k < n; ++k) {  // replicas are point-major, rep-minor: sums in rep order
+        const auto [p, rep] = b.replica_origin[k];
+        SweepPoint& pt = b.points[static_cast<size_t>(p)];
+        const dsd_replica_summary& s = sums[k];
+        tot.events += static_cast<double>(s.events_processed);
+        tot.replicas += 1;
+        if (s.status != DSD_OK) {
+            pt.failed = true;
+            pt.error = "engine capacity exceeded on the device (event heap / sequence arena)";
+            continue;
+        }
+        thr[p] += s.throughput_rps;
+        ttft[p] += s.mean_ttft_ms;
+        tpot[p] += s.mean_tpot_ms;
+        if (reports) {
+            const Resolved& r = b.resolved[static_cast<size_t>(b.point_scenario[p])];
+            ReplicaOutput out;
+            out.summary = s;
+            int64_t nrec = 0, nseq = 0;
+            rt.fetch_records(k, nullptr, 0, &nrec, nullptr, nullptr, 0, &nseq, nullptr, 0);
+            out.records.resize(static_cast<size_t>(nrec));
+            out.gamma_seq.resize(static_cast<size_t>(nseq));
+            out.committed_seq.resize(static_cast<size_t>(nseq));
+            out.busy_us.resize(static_cast<size_t>(r.scen.n_targets));
+            rt.fetch_records(k, out.records.data(), out.records.size(), &nrec, out.gamma_seq.data(),
+                             out.committed_seq.data(), out.gamma_seq.size(), &nseq, out.busy_us.data(),
+                             out.busy_us.size());
+            const std::string file =
+                out_dir + "/" + sanitize_filename(pt.point_id) + "_rep" + std::to_string(rep) + ".json";
+            std::ofstream f(file, std::ios::binary);
+            if (!f) throw Error(DSD_ERR_RUNTIME, "cannot write file: " + file);
+            f << emit_report(out, r.scen.n_targets, r.digest, b.replicas[k].seed);
+            pt.report_files.push_back(file);
+        }
+    }
+    for (size_t p = 0; p < b.points.size(); ++p) {
+        SweepPoint& pt = b.points[p];
+        tot.points += 1;
+        if (pt.failed) {
+            tot.failed += 1;
+            continue;
+        }
+        pt.mean_throughput_rps = thr[p] / R;
+        pt.mean_ttft_ms = ttft[p] / R;
+        pt.mean_tpot_ms = tpot[p] / R;
+    }
+    return tot;
+}
+
+std::string sweep_summary_json(const std::vector<SweepPoint>& points) {
+    JsonOut w;
+    w.open_object();
+    w.key("points").open_array();
+    for (const auto& p : points) {
+        w.open_object();
+        w.key("point").str(p.point_id);
+        w.key("assignment").open_object();
+        for (const auto& kv : p.assignment) w.key(kv.first).str(kv.second);
+        w.close_object();
+        w.key("failed").boolean(p.failed);
+        if (p.failed) {
+            w.key("error").str(p.error);
+        } else {
+            w.key("throughput_rps").fixed(p.mean_throughput_rps, 6);
+            w.key("mean_ttft_ms").fixed(p.mean_ttft_ms, 3);
+            w.key("mean_tpot_ms").fixed(p.mean_tpot_ms, 3);
+        }
+        w.close_object();
+    }
+    w.close_array();
+    w.close_object();
+    std::string out = w.take();
+    out += '\n';
+    return out;
+}
+
+std::string sweep_summary_csv(const std::vector<SweepPoint>& points) {
+    std::string out = "point,failed,throughput_rps,mean_ttft_ms,mean_tpot_ms\n";
+    for (const auto& p : points) {
+        out += "\"" + p.point_id + "\"," + (p.failed ? "1" : "0") + ',';
+        out += cfg::fmt_fixed(p.mean_throughput_rps, 6) + ',' + cfg::fmt_fixed(p.mean_ttft_ms, 3) + ',' +
+               cfg::fmt_fixed(p.mean_tpot_ms, 3) + '\n';
+    }
+    return out;
+}
+
+}  // namespace dsd::host

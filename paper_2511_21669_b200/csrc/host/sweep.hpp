@@ -1,0 +1,59 @@
+// sweep.hpp — the simulate-a-sweep driver on the GPU engine: SweepSpec
+// (proj/include/specsim/runner/sweep.hpp:17-50, proj/src/runner/sweep.cpp:16-199)
+// resolved once per point, all (point, repetition) replicas in one device batch.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../device/runtime.hpp"
+#include "resolve.hpp"
+#include "yaml.hpp"
+
+namespace dsd::host {
+
+struct SweepSpec {
+    cfg::Node base;
+    std::string base_dir;
+    uint64_t base_seed = 42;
+    int repetitions = 1;
+    std::vector<std::pair<std::string, std::vector<cfg::Node>>> axes;
+    static SweepSpec from_node(const cfg::Node& node, const std::string& base_dir);
+    size_t point_count() const;
+};
+
+struct SweepPoint {
+    std::vector<std::pair<std::string, std::string>> assignment;
+    std::string point_id;
+    bool failed = false;
+    std::string error;
+    double mean_throughput_rps = 0.0, mean_ttft_ms = 0.0, mean_tpot_ms = 0.0;
+    std::vector<std::string> report_files;
+};
+
+uint64_t sweep_point_seed(uint64_t base_seed, const std::string& point_id, int repetition);
+
+// Points resolved into scenarios + replicas (optionally one shard of them).
+struct SweepBatch {
+    SweepSpec spec;
+    std::vector<SweepPoint> points;
+    std::vector<Resolved> resolved;          // one per resolvable point
+    std::vector<int64_t> point_scenario;     // point -> index in resolved, -1 when failed
+    std::vector<dsd_scenario> scenarios;
+    std::vector<dsd_replica> replicas;
+    std::vector<std::pair<int64_t, int>> replica_origin;  // replica -> (point, rep)
+};
+
+SweepBatch plan_sweep(const cfg::Node& node, const std::string& base_dir, int shard, int n_shards, Caches* caches);
+
+struct SweepTotals {
+    double points = 0, replicas = 0, failed = 0, events = 0;
+};
+
+// run_sweep on the GPU; writes per-replica reports when out_dir is non-empty.
+SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir);
+std::string sweep_summary_json(const std::vector<SweepPoint>& points);
+std::string sweep_summary_csv(const std::vector<SweepPoint>& points);
+
+}  // namespace dsd::host

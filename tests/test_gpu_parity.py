@@ -1,0 +1,100 @@
+"""GPU parity: the sm_100a engine vs the reference simulator (oracle/_ref) on
+the same configs.  Bit-exact: every report byte (all integer outputs and the
+3/6-decimal float renderings), events_processed and end_time must match."""
+import os
+
+import pytest
+
+import reforacle as ref
+
+pytestmark = pytest.mark.gpu
+CFG = ref.CONFIGS
+
+
+def _cfg(name):
+    with open(os.path.join(CFG, name)) as f:
+        return f.read()
+
+
+def _compare(sim, text, base_dir=".", seed=None):
+    rep, ev, end, agg = ref.run_config(text, base_dir, seed)
+    out = sim.run_simulation(text, base_dir=base_dir, seed=seed)
+    assert out.events_processed == ev
+    assert out.end_time_us == end
+    if out.report_json != rep:
+        a, b = rep.splitlines(), out.report_json.splitlines()
+        for i, (x, y) in enumerate(zip(a, b)):
+            assert x == y, f"first report difference at line {i}"
+        assert len(a) == len(b)
+    assert out.completed == int(agg[0])
+    assert out.throughput_rps == agg[1]
+    assert out.mean_ttft_ms == agg[2]
+    assert out.mean_tpot_ms == agg[3]
+    return out
+
+
+@pytest.mark.parametrize("name,golden", [
+    ("c1_single_pair.yaml", "12253632ad5d73e55984bf1b64a17e8b4cb966f1c137e65367a1d78f228ed7ce"),
+    ("c2_8x1_batching.yaml", "cb0d409d66afb46dab47f25590fb30a3f8f6f88531bfd088b640837eb4bf90a1"),
+    ("c3_64x4_awc.yaml", "eb1dbe06b534b6e52dde1a7da752cf91abac9712e5005936bff30af8a197bdb3"),
+    ("c4_1024x16_static.yaml", "3b4a3e55b3f2f45bb5d613e107b06605735cd1ed21f102516c28a816b3bb156f"),
+    ("c4_1024x16_awc.yaml", None),
+])
+def test_baseline_configs_bit_exact(sim, gen_dir, name, golden):
+    out = _compare(sim, _cfg(name), gen_dir)
+    if golden:
+        assert ref.sha256(out.report_json) == golden
+
+
+VARIANTS = {
+    "rr_lab": [("routing: random", "routing: rr"), ("kind: fifo", "kind: lab")],
+    "jsq_dynamic": [("routing: random", "routing: jsq"), ("kind: static", "kind: dynamic")],
+    "fused": [("kind: static", "kind: fused")],
+    "jitter": [("jitter_ms: 0", "jitter_ms: 4")],
+    "window_us": [("max_batch_size: 8", "max_batch_size: 3\n    batching_window_us: 1500")],
+    "gen_seed": [("acceptance_rate: 0.8", "acceptance_rate: 0.3\n  gen_seed: 99")],
+    "preset": [("prompt_median: 32\n  output_median: 72", "preset: cnndm-like")],
+    "multi": [("targets: 1", "targets: 3"), ("drafts: 1", "drafts: 5"), ("routing: random", "routing: random"),
+              ("jitter_ms: 0", "jitter_ms: 3"), ("rate_rps: 2", "rate_rps: 9")],
+    "draft_batch": [("drafts: 1", "drafts: 4"), ("routing: random", "routing: jsq\n  draft_max_batch: 3")],
+}
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+def test_policy_variants_bit_exact(sim, variant):
+    text = _cfg("c1_single_pair.yaml")
+    for a, b in VARIANTS[variant]:
+        assert a in text
+        text = text.replace(a, b, 1)
+    _compare(sim, text)
+
+
+@pytest.mark.parametrize("seed", [1, 7, 123456789, 2**63 + 5])
+def test_seed_override(sim, seed):
+    _compare(sim, _cfg("c2_8x1_batching.yaml"), seed=seed)
+
+
+def test_trace_poisson_resampling(sim, gen_dir):
+    text = _cfg("c4_1024x16_static.yaml").replace("mode: trace", "mode: poisson\n  rate_rps: 80")
+    _compare(sim, text, gen_dir)
+
+
+def test_sweep_summary_matches_reference(sim):
+    spec = ("base: c2_8x1_batching.yaml\nseed: 7\nrepetitions: 3\naxes:\n"
+            "  network.rtt_ms: [0, 10, 50]\n  policies.window.kind: [static, fused, dynamic]\n"
+            "  policies.window.gamma: [2, 13]\n")
+    js, cs = ref.run_sweep(spec, CFG, 4)
+    out = sim.run_sweep(spec, base_dir=CFG)
+    assert out.summary_json == js
+    assert out.summary_csv == cs
+
+
+def test_sweep_report_files_match_reference(sim, tmp_path):
+    spec = "base: c1_single_pair.yaml\nseed: 3\nrepetitions: 2\naxes:\n  network.rtt_ms: [4, 30]\n"
+    ref_dir, my_dir = tmp_path / "ref", tmp_path / "mine"
+    ref.run_sweep(spec, CFG, 2, str(ref_dir))
+    sim.run_sweep(spec, base_dir=CFG, out_dir=str(my_dir))
+    ref_files = sorted(os.listdir(ref_dir))
+    assert ref_files == sorted(os.listdir(my_dir))
+    for f in ref_files:
+        assert (ref_dir / f).read_bytes() == (my_dir / f).read_bytes(), f
