@@ -246,6 +246,9 @@ int64_t dsd_last_launch_count(dsd_handle* h);
  * of the last launch (the dominant kernel) and of the whole launch. */
 int dsd_last_kernel_ms(dsd_handle* h, double* sim_kernel_ms, double* gen_kernel_ms,
                        double* total_ms);
+/* Host->device bytes of the last prepare (scenario blob + headers + replica
+ * table) and device->host bytes of the last summaries/records copy. */
+int dsd_last_transfer_bytes(dsd_handle* h, int64_t* h2d_bytes, int64_t* d2h_bytes);
 
 /* --- config-level entry points (the reference's C++ API, via YAML) -------- */
 

@@ -55,6 +55,7 @@ EXPORTS = [
     "dsd_abi_version", "dsd_create", "dsd_destroy", "dsd_run_batch", "dsd_fetch_records",
     "dsd_batch_prepare", "dsd_batch_launch", "dsd_batch_sync", "dsd_batch_summaries",
     "dsd_batch_device_summaries", "dsd_stream", "dsd_last_launch_count", "dsd_last_kernel_ms",
+    "dsd_last_transfer_bytes",
     "dsd_run_simulation", "dsd_run_sweep", "dsd_prepare_sweep", "dsd_resolve_config", "dsd_resolved_scenario",
     "dsd_resolved_replica", "dsd_resolved_digest", "dsd_resolved_free", "dsd_plan_sweep",
     "dsd_sweep_plan_scenarios", "dsd_sweep_plan_replicas", "dsd_sweep_plan_free", "dsd_emit_report",
@@ -96,6 +97,7 @@ def lib():
     L.dsd_last_launch_count.argtypes = [vp]
     L.dsd_last_launch_count.restype = c.c_int64
     L.dsd_last_kernel_ms.argtypes = [vp, c.POINTER(c.c_double), c.POINTER(c.c_double), c.POINTER(c.c_double)]
+    L.dsd_last_transfer_bytes.argtypes = [vp, c.POINTER(c.c_int64), c.POINTER(c.c_int64)]
     L.dsd_run_simulation.argtypes = [vp, cp, cp, c.c_int, c.c_int, c.c_uint64, c.POINTER(vp), c.POINTER(vp),
                                      c.POINTER(c.c_uint64), c.POINTER(c.c_int64), c.POINTER(c.c_double), cp, sz]
     L.dsd_run_sweep.argtypes = [vp, cp, cp, cp, c.POINTER(vp), c.POINTER(vp), c.POINTER(c.c_double), cp, sz]

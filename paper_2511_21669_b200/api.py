@@ -196,6 +196,11 @@ class Simulator:
     def last_launch_count(self) -> int:
         return int(self._L.dsd_last_launch_count(self._h))
 
+    def last_transfer_bytes(self):
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        self._L.dsd_last_transfer_bytes(self._h, ctypes.byref(a), ctypes.byref(b))
+        return a.value, b.value
+
     def last_kernel_ms(self):
         a, b, t = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         self._L.dsd_last_kernel_ms(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(t))

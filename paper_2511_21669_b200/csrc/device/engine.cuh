@@ -13,8 +13,10 @@
 //  * work queues, running batches and draft session FIFOs are intrusive
 //    linked lists through two work-item slots per request (a target prefill
 //    and "the other" item), so no per-server capacity is needed;
-//  * replica scalars (clock, seq counter, RNG states, totals) live in
-//    registers for the whole run; everything else is warp-interleaved SoA.
+//  * replica scalars (clock, seq counter, RNG states, totals, the action
+//    stack) live in registers for the whole run; per-request state is one
+//    128-byte record per request; server state and the event heap are
+//    warp-interleaved SoA (a warp's 32 replicas read one row per slot).
 // Bit-exactness: all floating point is compiled with -fmad=false and follows
 // the reference's operation order (see comments at each site).
 #pragma once
@@ -54,6 +56,20 @@ DSD_HD int segment_index(const double* axis, int n, double q) {
     if (lo == 0) return 0;
     if (lo >= n) return n - 2;
     return lo - 1;
+}
+
+// Same result as grid_interpolate(blob, g, qb, qc) for integer queries, from
+// the host-built segment tables: two table loads instead of two binary
+// searches and two divisions.
+DSD_HD double grid_interpolate_int(const char* blob, const DevGrid& g, int64_t qb, int64_t qc) {
+    const AxisSeg sb = blob_ptr<AxisSeg>(blob, g.o_btab)[qb < g.nbt ? qb : g.nbt - 1];
+    const AxisSeg sc = blob_ptr<AxisSeg>(blob, g.o_ctab)[qc < g.nct ? qc : g.nct - 1];
+    const double* v = blob_ptr<double>(blob, g.o_vals);
+    const int n = g.nc;
+    const double tb = sb.t, tc = sc.t;
+    double r = (1.0 - tb) * (1.0 - tc) * v[sb.lo * n + sc.lo] + (1.0 - tb) * tc * v[sb.lo * n + sc.hi] +
+               tb * (1.0 - tc) * v[sb.hi * n + sc.lo] + tb * tc * v[sb.hi * n + sc.hi];
+    return r * g.calibration;
 }
 
 DSD_HD double grid_interpolate(const char* blob, const DevGrid& g, double batch, double context) {
@@ -100,7 +116,9 @@ DSD_HD void matvec_avx2_order(const double* w, const double* x, const double* bi
     }
 }
 
-DSD_HD double awc_predict(const char* blob, const DevScenario& S, const double raw[5]) {
+// out of line: ~34K flops per call, called once per AWC decision; keeping it
+// out of the event loop keeps the loop small enough for the instruction cache
+DSD_HD_NOINLINE double awc_predict(const char* blob, const DevScenario& S, const double raw[5]) {
     double x[5];
     for (int f = 0; f < 5; ++f) {
         double v = S.awc_log[f] ? log1p(raw[f]) : raw[f];
@@ -135,18 +153,51 @@ DSD_HD double awc_predict(const char* blob, const DevScenario& S, const double r
 
 // ---------------------------------------------------------------------------
 // the engine
+//
+// Control flow is continuation-passing: the reference's nested call chains
+// (push_work -> try_dispatch, finish_request -> activate_next_session ->
+// push_work, on_compute_done's per-item loop, ...) become small actions on a
+// 4-deep register stack that the main loop pops before it takes the next
+// event.  Every handler body therefore exists exactly once in the binary
+// (the fully inlined direct-call version was ~28K SASS instructions and
+// stalled on instruction fetch), and all schedule() calls still happen in the
+// reference's order, so seq numbers - and with them the (time, seq) event
+// order - are identical.  The deepest chain (compute-done item -> finish ->
+// activate -> dispatch) needs 3 stack slots.
 // ---------------------------------------------------------------------------
+// Kinds are numbered in the order they follow each other inside one event's
+// chain (pop -> handler -> ... -> dispatch -> send prompt), so the kernel's
+// cyclic sweep over kinds usually carries a lane through a whole event per sweep.
+enum : uint32_t {
+    kActPop = 0,          // pop the next event (stack empty)
+    kActArrival = 1,      // on_arrival(i)                     arg = i
+    kActNetPrompt = 2,    // NetArrive handlers, by message:   arg = i
+    kActNetProposal = 3,  //   kActNetPrompt + kMsg*
+    kActNetResult = 4,
+    kActBegin = 5,        // [decide_window] + begin_iteration  arg = i*2 + decide
+    kActComputeDone = 6,  // on_compute_done(v)                arg = v
+    kActItem = 7,         // one item of a finished batch      arg = slot
+    kActFinish = 8,       // finish_request(i)                 arg = i
+    kActActivate = 9,     // activate_next_session(d)          arg = d
+    kActDispatch = 10,    // try_dispatch(v, expired)          arg = v*2 + expired
+    kActSendPrompt = 11,  // ship the prompt to the verifier   arg = i
+    kActKinds = 12,
+    kActNone = 15         // replica finished
+};
+// Actions are kind | arg << 4 (args < 2^28: requests < 2^26, slots < 2^27).
+
 struct Engine {
     const Workspace& W;
     const DevScenario& S;
     const char* blob;
     Lane L;
     int64_t rep;
+    ReqRec* R;  // this replica's request records
 
     // replica scalars (registers)
     int64_t N;
     int64_t now = 0;
-    uint32_t seq_next;      // next seq for schedule(); arrivals hold 0..N-1
+    uint32_t seq_next;  // next seq for schedule(); arrivals hold 0..N-1
     int64_t heap_n = 0;
     int64_t next_arr = 0;
     uint64_t processed = 0;
@@ -158,41 +209,94 @@ struct Engine {
     int32_t fail = kFailNone;
     int64_t seqbase = 0;
     int32_t T, D;
+    // action stack
+    uint32_t st0 = 0, st1 = 0, st2 = 0, st3 = 0;
+    int sp = 0;
+    int32_t item_server = -1;
+    // per-warp state blocks (shared memory for small topologies, else HBM),
+    // already offset by this lane: element k of a field is at base[k * 32]
+    int32_t* sb;     // server fields [kServerFields][nsc]
+    int64_t* htb;    // heap times [hcap]
+    uint64_t* hkb;   // heap keys  [hcap]
+    int64_t hcap;
+    int32_t nsc;
+    // hot scenario parameters held in registers
+    int32_t fe, ps, wkind, gamma_s, max_batch, dmax_batch, batching, routing_kind;
+    int64_t win_us;
+    double sim_frac;
 
-    DSD_HD Engine(const Workspace& w, const DevScenario& s, int64_t replica)
-        : W(w), S(s), blob(w.blob), rep(replica) {
+    DSD_HD Engine(const Workspace& w, const DevScenario& s, int64_t replica, int32_t* server_base,
+                  int64_t* heap_time_base, uint64_t* heap_key_base, int64_t heap_cap, int32_t server_cap)
+        : W(w), S(s), blob(w.blob), rep(replica), sb(server_base), htb(heap_time_base), hkb(heap_key_base),
+          hcap(heap_cap), nsc(server_cap) {
         L.w = replica / kLanes;
         L.lane = static_cast<int>(replica % kLanes);
         T = S.n_targets;
         D = S.n_drafts;
+        R = W.req + replica * W.c.nr;
+        fe = S.fused_everything;
+        ps = S.pair_stats;
+        wkind = S.window_kind;
+        gamma_s = S.gamma;
+        max_batch = S.max_batch;
+        dmax_batch = S.draft_max_batch;
+        batching = S.batching;
+        routing_kind = S.routing;
+        win_us = S.batching_window_us;
+        sim_frac = S.sim_frac;
     }
 
-    // ---- accessors ----
-    DSD_HD int64_t nr() const { return W.c.nr; }
-#define RQ(field, i) L.at(W.field, W.c.nr, (i))
-#define SL(field, i) L.at(W.field, 2 * W.c.nr, (i))
-#define SV(field, i) L.at(W.field, W.c.ns, (i))
+    // server fields (engine.cpp:70-84 Server, minus the queue/running vectors
+    // which are intrusive lists through the request records)
+    enum : int {
+        F_v_qhead = 0, F_v_qtail, F_v_run, F_v_busy, F_v_armed, F_v_armseq, F_v_active, F_v_shead, F_v_stail,
+        F_v_open
+    };
+#define SV(field, i) sv(F_##field, (i))
+    DSD_HD int32_t& sv(int f, int32_t v) const { return sb[(static_cast<int64_t>(f) * nsc + v) * kLanes]; }
+    DSD_HD int64_t& busy_us(int32_t v) const { return L.at(W.v_busy_us, W.c.ns, v); }
+    DSD_HD int64_t& ht(int64_t k) const { return htb[k * kLanes]; }
+    DSD_HD uint64_t& hk(int64_t k) const { return hkb[k * kLanes]; }
 
-    DSD_HD uint32_t phase(int64_t i) const { return RQ(r_flags, i) & 7u; }
-    DSD_HD void set_phase(int64_t i, uint32_t p) {
-        uint8_t& f = RQ(r_flags, i);
-        f = static_cast<uint8_t>((f & ~7u) | p);
+    // ---- action stack ----
+    static DSD_HD uint32_t act(uint32_t kind, uint32_t arg) { return kind | (arg << 4); }
+    DSD_HD void push_act(uint32_t a) {
+        if (sp >= 4) {
+            fail = kFailStack;
+            return;
+        }
+        st3 = st2;
+        st2 = st1;
+        st1 = st0;
+        st0 = a;
+        ++sp;
     }
-    DSD_HD bool flag(int64_t i, int bit) const { return (RQ(r_flags, i) >> bit) & 1u; }
-    DSD_HD void set_flag(int64_t i, int bit, bool v) {
-        uint8_t& f = RQ(r_flags, i);
-        f = static_cast<uint8_t>(v ? (f | (1u << bit)) : (f & ~(1u << bit)));
+    DSD_HD uint32_t pop_act() {
+        uint32_t a = st0;
+        st0 = st1;
+        st1 = st2;
+        st2 = st3;
+        --sp;
+        return a;
     }
+
+    // ---- request flags ----
     static constexpr int kDpd = 3, kTpd = 4, kFused = 5;
-
-    DSD_HD int32_t draft_of(int64_t i) const { return D > 0 ? RQ(r_drafter, i) : -1; }
+    DSD_HD uint32_t phase(int64_t i) const { return R[i].flags & 7u; }
+    DSD_HD void set_phase(int64_t i, uint32_t p) { R[i].flags = static_cast<uint8_t>((R[i].flags & ~7u) | p); }
+    DSD_HD bool flag(int64_t i, int bit) const { return (R[i].flags >> bit) & 1u; }
+    DSD_HD void set_flag(int64_t i, int bit, bool v) {
+        uint8_t f = R[i].flags;
+        R[i].flags = static_cast<uint8_t>(v ? (f | (1u << bit)) : (f & ~(1u << bit)));
+    }
+    DSD_HD int32_t draft_of(int64_t i) const { return D > 0 ? R[i].drafter : -1; }
 
     // ---- event heap: SimKernel::schedule (event_queue.cpp:20-26) ----
-    DSD_HD bool key_less(int64_t ta, uint64_t ka, int64_t tb, uint64_t kb) const {
+    static DSD_HD bool key_less(int64_t ta, uint64_t ka, int64_t tb, uint64_t kb) {
         return ta < tb || (ta == tb && ka < kb);
     }
     DSD_HD void schedule(int64_t t, uint32_t info) {
-        if (heap_n >= W.c.hc) {
+        if (heap_n >= hcap) {
             fail = kFailHeap;
             return;
         }
@@ -201,30 +305,30 @@ struct Engine {
         int64_t i = heap_n++;
         while (i > 0) {
             int64_t p = (i - 1) >> 1;
-            int64_t pt = L.at(W.h_time, W.c.hc, p);
-            uint64_t pk = L.at(W.h_key, W.c.hc, p);
+            int64_t pt = ht(p);
+            uint64_t pk = hk(p);
             if (!key_less(t, key, pt, pk)) break;
-            L.at(W.h_time, W.c.hc, i) = pt;
-            L.at(W.h_key, W.c.hc, i) = pk;
+            ht(i) = pt;
+            hk(i) = pk;
             i = p;
         }
-        L.at(W.h_time, W.c.hc, i) = t;
-        L.at(W.h_key, W.c.hc, i) = key;
+        ht(i) = t;
+        hk(i) = key;
     }
     DSD_HD void heap_pop() {
         int64_t n = --heap_n;
         if (n == 0) return;
-        int64_t t = L.at(W.h_time, W.c.hc, n);
-        uint64_t k = L.at(W.h_key, W.c.hc, n);
+        int64_t t = ht(n);
+        uint64_t k = hk(n);
         int64_t i = 0;
         for (;;) {
             int64_t c = 2 * i + 1;
             if (c >= n) break;
-            int64_t ct = L.at(W.h_time, W.c.hc, c);
-            uint64_t ck = L.at(W.h_key, W.c.hc, c);
+            int64_t ct = ht(c);
+            uint64_t ck = hk(c);
             if (c + 1 < n) {
-                int64_t dt = L.at(W.h_time, W.c.hc, c + 1);
-                uint64_t dk = L.at(W.h_key, W.c.hc, c + 1);
+                int64_t dt = ht(c + 1);
+                uint64_t dk = hk(c + 1);
                 if (key_less(dt, dk, ct, ck)) {
                     c = c + 1;
                     ct = dt;
@@ -232,38 +336,32 @@ struct Engine {
                 }
             }
             if (!key_less(ct, ck, t, k)) break;
-            L.at(W.h_time, W.c.hc, i) = ct;
-            L.at(W.h_key, W.c.hc, i) = ck;
+            ht(i) = ct;
+            hk(i) = ck;
             i = c;
         }
-        L.at(W.h_time, W.c.hc, i) = t;
-        L.at(W.h_key, W.c.hc, i) = k;
+        ht(i) = t;
+        hk(i) = k;
     }
-
-    static DSD_HD uint32_t info(uint32_t kind, uint32_t msg, uint32_t id) {
-        return kind | (msg << 3) | (id << 5);
-    }
+    static DSD_HD uint32_t info(uint32_t kind, uint32_t msg, uint32_t id) { return kind | (msg << 3) | (id << 5); }
 
     // ---- network: net_delay (engine.cpp:10-15) ----
-    DSD_HD int64_t net_delay(int32_t d, int32_t t) {
+    DSD_HD const double* link(int32_t d, int32_t t) const {
         const int32_t* dg = blob_ptr<int32_t>(blob, S.o_dgroup);
         const int32_t* tg = blob_ptr<int32_t>(blob, S.o_tgroup);
-        const double* lk = blob_ptr<double>(blob, S.o_links) + 2 * (dg[d] * S.n_tg + tg[t]);
+        return blob_ptr<double>(blob, S.o_links) + 2 * (dg[d] * S.n_tg + tg[t]);
+    }
+    DSD_HD int64_t net_delay(int32_t d, int32_t t) {
+        const double* lk = link(d, t);
         double rtt = lk[0], jit = lk[1];
         double j = jitter.uniform(-jit / 2.0, jit / 2.0);
         double ms = rtt / 2.0 + j;
         if (ms < 0.0) ms = 0.0;
         return llround(ms * 1000.0);
     }
-    DSD_HD double link_rtt(int32_t d, int32_t t) const {
-        const int32_t* dg = blob_ptr<int32_t>(blob, S.o_dgroup);
-        const int32_t* tg = blob_ptr<int32_t>(blob, S.o_tgroup);
-        return blob_ptr<double>(blob, S.o_links)[2 * (dg[d] * S.n_tg + tg[t])];
-    }
 
     // ---- metrics hooks (metrics.cpp:40-128) ----
     DSD_HD int64_t pair_of(int32_t d, int32_t t) const { return static_cast<int64_t>(d) * T + t; }
-
     DSD_HD double acceptance_recent(int64_t p) const {
         int32_t cnt = L.at(W.p_acc_cnt, W.c.np, p);
         int64_t ex = 0, ac = 0;
@@ -274,50 +372,29 @@ struct Engine {
         if (ex == 0) return 0.5;
         return static_cast<double>(ac) / static_cast<double>(ex);
     }
+    // fixed-capacity ring insert: returns the storage slot (metrics.cpp:55-72)
+    static DSD_HD int64_t ring_slot(int32_t& cnt, int32_t& pos, int cap) {
+        if (cnt < cap) return cnt++;
+        int64_t s = pos;
+        pos = (pos + 1) % cap;
+        return s;
+    }
     DSD_HD void on_verify(int32_t d, int32_t t, int ex, int ac) {
-        if (!S.pair_stats) return;
+        if (!ps) return;
         int64_t p = pair_of(d, t);
-        int32_t& cnt = L.at(W.p_acc_cnt, W.c.np, p);
-        int32_t& pos = L.at(W.p_acc_pos, W.c.np, p);
-        int64_t slot;
-        if (cnt < 20) {
-            slot = cnt++;
-        } else {
-            slot = pos;
-            pos = (pos + 1) % 20;
-        }
+        int64_t slot = ring_slot(L.at(W.p_acc_cnt, W.c.np, p), L.at(W.p_acc_pos, W.c.np, p), 20);
         L.at(W.p_acc_ex, W.c.np * 20, p * 20 + slot) = ex;
         L.at(W.p_acc_ac, W.c.np * 20, p * 20 + slot) = ac;
     }
     DSD_HD void on_rtt_sample(int32_t d, int32_t t, double rtt_ms) {
-        if (!S.pair_stats) return;
+        if (!ps) return;
         int64_t p = pair_of(d, t);
-        int32_t& cnt = L.at(W.p_rtt_cnt, W.c.np, p);
-        int32_t& pos = L.at(W.p_rtt_pos, W.c.np, p);
-        int64_t slot;
-        if (cnt < 20) {
-            slot = cnt++;
-        } else {
-            slot = pos;
-            pos = (pos + 1) % 20;
-        }
+        int64_t slot = ring_slot(L.at(W.p_rtt_cnt, W.c.np, p), L.at(W.p_rtt_pos, W.c.np, p), 20);
         L.at(W.p_rtt, W.c.np * 20, p * 20 + slot) = rtt_ms;
     }
-    DSD_HD void on_gamma_chosen(int32_t d, int32_t t, int g) {
-        if (!S.pair_stats) return;
-        L.at(W.p_gprev, W.c.np, pair_of(d, t)) = g;
-    }
     DSD_HD void push_tpot(int32_t t, double v) {
-        if (!S.pair_stats) return;
-        int32_t& cnt = L.at(W.t_tcnt, W.c.nt, t);
-        int32_t& pos = L.at(W.t_tpos, W.c.nt, t);
-        int64_t slot;
-        if (cnt < 50) {
-            slot = cnt++;
-        } else {
-            slot = pos;
-            pos = (pos + 1) % 50;
-        }
+        if (!ps) return;
+        int64_t slot = ring_slot(L.at(W.t_tcnt, W.c.nt, t), L.at(W.t_tpos, W.c.nt, t), 50);
         L.at(W.t_tpot, W.c.nt * 50, static_cast<int64_t>(t) * 50 + slot) = v;
     }
 
@@ -329,10 +406,10 @@ struct Engine {
     DSD_HD Decision decide_window(int64_t i) {
         int32_t d = draft_of(i);
         if (d < 0) return Decision{true, 1};
-        int32_t t = RQ(r_target, i);
-        switch (S.window_kind) {
+        int32_t t = R[i].target;
+        switch (wkind) {
             case 0:  // window_static (policies.cpp:55-58)
-                return Decision{false, S.gamma};
+                return Decision{false, gamma_s};
             case 1: {  // window_dynamic (policies.cpp:60-68)
                 int64_t p = pair_of(d, t);
                 double a = acceptance_recent(p);
@@ -353,7 +430,7 @@ struct Engine {
                 f[1] = acceptance_recent(p);
                 int32_t rc = L.at(W.p_rtt_cnt, W.c.np, p);
                 if (rc == 0) {
-                    f[2] = link_rtt(d, t);
+                    f[2] = link(d, t)[0];
                 } else {
                     double sum = 0.0;
                     for (int k = 0; k < rc; ++k) sum += L.at(W.p_rtt, W.c.np * 20, p * 20 + k);
@@ -364,8 +441,7 @@ struct Engine {
                     f[3] = 0.0;
                 } else {
                     double sum = 0.0;
-                    for (int k = 0; k < tc; ++k)
-                        sum += L.at(W.t_tpot, W.c.nt * 50, static_cast<int64_t>(t) * 50 + k);
+                    for (int k = 0; k < tc; ++k) sum += L.at(W.t_tpot, W.c.nt * 50, static_cast<int64_t>(t) * 50 + k);
                     f[3] = sum / static_cast<double>(tc);
                 }
                 f[4] = static_cast<double>(L.at(W.p_gprev, W.c.np, p));
@@ -407,31 +483,31 @@ struct Engine {
         }
     }
 
-    // ---- work queues (intrusive lists through item slots) ----
-    DSD_HD void push_item(int32_t v, int64_t slot, uint32_t op, int32_t tokens, bool via) {
-        SL(s_op, slot) = static_cast<uint8_t>(op | (via ? 4u : 0u));
-        SL(s_tok, slot) = tokens;
-        SL(s_enq, slot) = now;
-        SL(s_next, slot) = -1;
+    // ---- work queues: intrusive lists through the records' item slots ----
+    DSD_HD int32_t slot_next(int32_t s) const { return R[s >> 1].next[s & 1]; }
+    DSD_HD void set_slot_next(int32_t s, int32_t n) { R[s >> 1].next[s & 1] = n; }
+
+    // push_work (engine.cpp:473-476): append, then try_dispatch as the next action
+    DSD_HD void enqueue(int32_t v, int64_t i, int k, uint32_t op, int32_t tokens, bool via) {
+        ReqRec& r = R[i];
+        r.op[k] = static_cast<uint8_t>(op | (via ? 4u : 0u));
+        if (k) r.tok1 = tokens;
+        r.enq[k] = now;
+        r.next[k] = -1;
+        const int32_t slot = static_cast<int32_t>(2 * i + k);
         int32_t& tail = SV(v_qtail, v);
         if (tail < 0) {
-            SV(v_qhead, v) = static_cast<int32_t>(slot);
+            SV(v_qhead, v) = slot;
         } else {
-            SL(s_next, tail) = static_cast<int32_t>(slot);
+            set_slot_next(tail, slot);
         }
-        tail = static_cast<int32_t>(slot);
-        try_dispatch(v, false);  // push_work (engine.cpp:473-476)
+        tail = slot;
+        push_act(act(kActDispatch, static_cast<uint32_t>(v) * 2));
     }
 
     DSD_HD bool eligible(bool is_draft, uint32_t op, int64_t req) const {
         // item_eligible (engine.cpp:478-483)
         return is_draft || op == kOpPrefill || flag(req, kTpd);
-    }
-
-    DSD_HD int64_t work_len(uint32_t op, int64_t slot) const {
-        if (op == kOpPrefill) return SL(s_tok, slot);
-        int64_t req = slot >> 1;
-        return static_cast<int64_t>(RQ(r_output, req)) - RQ(r_tokens, req);
     }
 
     // try_dispatch (engine.cpp:485-567)
@@ -440,49 +516,51 @@ struct Engine {
         const bool is_draft = v >= T;
         int32_t kind = -1;
         int64_t ncand = 0;
-        for (int32_t cur = SV(v_qhead, v); cur >= 0; cur = SL(s_next, cur)) {
-            uint32_t op = SL(s_op, cur) & 3u;
+        for (int32_t cur = SV(v_qhead, v); cur >= 0; cur = slot_next(cur)) {
+            uint32_t op = R[cur >> 1].op[cur & 1] & 3u;
             if (!eligible(is_draft, op, cur >> 1)) continue;
             if (kind < 0) kind = static_cast<int32_t>(op);
             if (static_cast<int32_t>(op) != kind) continue;
             ++ncand;
         }
         if (ncand == 0) return;
-        const int64_t max_batch = is_draft ? S.draft_max_batch : S.max_batch;
-        if (!is_draft && S.batching_window_us > 0 && !window_expired && ncand < max_batch) {
+        const int64_t mb = is_draft ? dmax_batch : max_batch;
+        if (!is_draft && win_us > 0 && !window_expired && ncand < mb) {
             if (!SV(v_armed, v)) {
                 SV(v_armed, v) = 1;
                 SV(v_armseq, v) = seq_next;  // stands in for ++window_gen (engine.cpp:512-517)
-                schedule(now + S.batching_window_us, info(kEvBatchReady, 0, static_cast<uint32_t>(v)));
+                schedule(now + win_us, info(kEvBatchReady, 0, static_cast<uint32_t>(v)));
             }
             return;
         }
         SV(v_armed, v) = 0;
 
-        const bool lab = !is_draft && S.batching == 1;
+        const bool lab = !is_draft && batching == 1;
         int64_t head_len = 0;
         double band = 0.0;
-        int64_t taken = 0;
-        int64_t seen = 0;
-        int32_t prev = -1;
-        int32_t run_tail = -1;
+        int64_t taken = 0, seen = 0;
+        int32_t prev = -1, run_tail = -1;
         int32_t tok = 1;
         int64_t ctx = 0;
         for (int32_t cur = SV(v_qhead, v); cur >= 0;) {
-            int32_t nxt = SL(s_next, cur);
-            uint32_t opv = SL(s_op, cur);
-            uint32_t op = opv & 3u;
+            const int64_t i = cur >> 1;
+            const int k = cur & 1;
+            ReqRec& r = R[i];
+            const int32_t nxt = r.next[k];
+            const uint32_t opv = r.op[k];
+            const uint32_t op = opv & 3u;
             bool take = false;
-            if (static_cast<int32_t>(op) == kind && eligible(is_draft, op, cur >> 1)) {
+            if (static_cast<int32_t>(op) == kind && eligible(is_draft, op, i)) {
                 if (!lab) {  // batch_fifo (policies.cpp:30-38)
-                    take = taken < max_batch;
-                } else {  // batch_lab (policies.cpp:40-53)
-                    int64_t wl = work_len(op, cur);
+                    take = taken < mb;
+                } else {     // batch_lab (policies.cpp:40-53)
+                    int64_t wl = op == kOpPrefill ? static_cast<int64_t>(k ? r.tok1 : r.prompt)
+                                                  : static_cast<int64_t>(r.output) - r.tokens;
                     if (seen == 0) {
                         head_len = wl;
-                        band = S.sim_frac * static_cast<double>(head_len);
+                        band = sim_frac * static_cast<double>(head_len);
                         take = true;
-                    } else if (taken < max_batch) {
+                    } else if (taken < mb) {
                         double diff = fabs(static_cast<double>(wl - head_len));
                         take = diff <= band;
                     }
@@ -491,23 +569,21 @@ struct Engine {
             }
             if (take) {
                 ++taken;
-                // unlink from the queue (stable removal)
-                if (prev < 0) SV(v_qhead, v) = nxt; else SL(s_next, prev) = nxt;
+                // stable removal from the queue, append to the running batch
+                if (prev < 0) SV(v_qhead, v) = nxt; else set_slot_next(prev, nxt);
                 if (SV(v_qtail, v) == cur) SV(v_qtail, v) = prev;
-                // append to the running batch
-                SL(s_next, cur) = -1;
-                if (run_tail < 0) SV(v_run, v) = cur; else SL(s_next, run_tail) = cur;
+                r.next[k] = -1;
+                if (run_tail < 0) SV(v_run, v) = cur; else set_slot_next(run_tail, cur);
                 run_tail = cur;
                 // BatchShape (engine.cpp:544-552)
-                int32_t t_i = SL(s_tok, cur);
+                int32_t t_i = k ? r.tok1 : r.prompt;
                 if (t_i > tok) tok = t_i;
                 if (op != kOpPrefill) {
-                    int64_t req = cur >> 1;
-                    int64_t c = static_cast<int64_t>(RQ(r_prompt, req)) + RQ(r_tokens, req);
+                    int64_t c = static_cast<int64_t>(r.prompt) + r.tokens;
                     if (c > ctx) ctx = c;
                 }
                 if (opv & 4u) {
-                    net_wait_total += now - SL(s_enq, cur);
+                    net_wait_total += now - r.enq[k];
                     ++net_wait_count;
                 }
             } else {
@@ -519,41 +595,39 @@ struct Engine {
         const int32_t* gi = is_draft ? blob_ptr<int32_t>(blob, S.o_dgrid) + 2 * (v - T)
                                      : blob_ptr<int32_t>(blob, S.o_tgrid) + 2 * v;
         const DevGrid* grids = blob_ptr<DevGrid>(blob, S.o_grids);
-        double ms;
-        if (kind == static_cast<int32_t>(kOpPrefill)) {
-            ms = grid_interpolate(blob, grids[gi[0]], static_cast<double>(taken),
-                                  static_cast<double>(tok));
-        } else if (kind == static_cast<int32_t>(kOpDecode)) {
-            ms = grid_interpolate(blob, grids[gi[1]], static_cast<double>(taken),
-                                  static_cast<double>(ctx));
-            ms *= tok;
-        } else {
-            ms = grid_interpolate(blob, grids[gi[1]], static_cast<double>(taken) * tok,
-                                  static_cast<double>(ctx));
-        }
+        const bool prefill = kind == static_cast<int32_t>(kOpPrefill);
+        const bool decode = kind == static_cast<int32_t>(kOpDecode);
+        // queries: (batch, prompt tokens) / (batch, context) / (batch*tokens, context)
+        const int64_t qb = (prefill || decode) ? taken : taken * tok;
+        const int64_t qc = prefill ? static_cast<int64_t>(tok) : ctx;
+        const DevGrid& g = grids[gi[prefill ? 0 : 1]];
+        double ms = g.o_btab >= 0 && g.o_ctab >= 0
+                        ? grid_interpolate_int(blob, g, qb, qc)
+                        : grid_interpolate(blob, g, static_cast<double>(qb), static_cast<double>(qc));
+        if (decode) ms *= tok;
         int64_t lat = llround(ms * 1000.0);
         if (lat < 1) lat = 1;
         SV(v_busy, v) = 1;
-        SV(v_busy_us, v) += lat;
+        busy_us(v) += lat;
         schedule(now + lat, info(kEvComputeDone, 0, static_cast<uint32_t>(v)));
     }
 
     // ---- request lifecycle ----
     DSD_HD void record_gamma(int64_t i, int g) {
-        int32_t& n = RQ(r_ng, i);
+        int32_t n = R[i].ng;
         if (W.collect) {
-            int64_t o = seqbase + RQ(r_seqoff, i) + n;
+            int64_t o = seqbase + R[i].seqoff + n;
             if (o < W.seq_cap) W.seq_gamma[o] = g; else fail = kFailSeq;
         }
-        ++n;
+        R[i].ng = n + 1;
     }
     DSD_HD void record_commit(int64_t i, int c) {
-        int32_t& n = RQ(r_nc, i);
+        int32_t n = R[i].nc;
         if (W.collect) {
-            int64_t o = seqbase + RQ(r_seqoff, i) + n;
+            int64_t o = seqbase + R[i].seqoff + n;
             if (o < W.seq_cap) W.seq_commit[o] = c; else fail = kFailSeq;
         }
-        ++n;
+        R[i].nc = n + 1;
     }
 
     // activate_next_session (engine.cpp:332-339)
@@ -561,15 +635,16 @@ struct Engine {
         int32_t v = T + d;
         if (SV(v_active, v) >= 0 || SV(v_shead, v) < 0) return;
         int32_t i = SV(v_shead, v);
-        SV(v_shead, v) = RQ(r_snext, i);
-        if (SV(v_shead, v) < 0) SV(v_stail, v) = -1;
+        int32_t nx = R[i].snext;
+        SV(v_shead, v) = nx;
+        if (nx < 0) SV(v_stail, v) = -1;
         SV(v_active, v) = i;
-        push_item(v, 2 * static_cast<int64_t>(i) + 1, kOpPrefill, RQ(r_prompt, i), false);
+        enqueue(v, i, 1, kOpPrefill, R[i].prompt, false);
     }
 
     // route (engine.cpp:315-330, policies.cpp:9-28)
     DSD_HD int32_t route() {
-        switch (S.routing) {
+        switch (routing_kind) {
             case 0:
                 return static_cast<int32_t>(routing.below(static_cast<uint64_t>(T)));
             case 1:
@@ -591,61 +666,58 @@ struct Engine {
 
     // on_arrival (engine.cpp:289-313)
     DSD_HD void on_arrival(int64_t i) {
-        RQ(r_arrival, i) = now;
         set_phase(i, kPhRouted);
         int32_t t = route();
-        RQ(r_target, i) = t;
+        R[i].target = t;
         ++SV(v_open, t);  // MetricsCollector::on_route
         if (first_arrival < 0 || now < first_arrival) first_arrival = now;
         set_phase(i, kPhQueuedPrefill);
-        if (S.fused_everything) {
+        if (fe) {
             set_flag(i, kFused, true);
-            push_item(t, 2 * i, kOpPrefill, RQ(r_prompt, i), false);
+            enqueue(t, i, 0, kOpPrefill, R[i].prompt, false);
         } else {
-            int32_t d = RQ(r_drafter, i);
+            int32_t d = R[i].drafter;
             int32_t v = T + d;
-            RQ(r_snext, i) = -1;
+            R[i].snext = -1;
             int32_t tail = SV(v_stail, v);
-            if (tail < 0) SV(v_shead, v) = static_cast<int32_t>(i); else RQ(r_snext, tail) = static_cast<int32_t>(i);
+            if (tail < 0) SV(v_shead, v) = static_cast<int32_t>(i); else R[tail].snext = static_cast<int32_t>(i);
             SV(v_stail, v) = static_cast<int32_t>(i);
-            activate_next_session(d);
-            int64_t delay = net_delay(d, t);
-            schedule(now + delay, info(kEvNetArrive, kMsgPrompt, static_cast<uint32_t>(i)));
+            // activate_next_session runs first, then net_delay + schedule
+            push_act(act(kActSendPrompt, static_cast<uint32_t>(i)));
+            push_act(act(kActActivate, static_cast<uint32_t>(d)));
         }
     }
 
-    // begin_iteration (engine.cpp:383-404)
-    DSD_HD void begin_iteration(int64_t i, Decision dec) {
+    // [decide_window] + begin_iteration (engine.cpp:254-257, 383-404)
+    DSD_HD void begin(int64_t i, bool decide) {
+        Decision dec = decide ? decide_window(i) : Decision{true, 1};
         if (phase(i) == kPhDone) return;
         int32_t d = draft_of(i);
-        int32_t t = RQ(r_target, i);
-        if (d >= 0 && t >= 0) on_gamma_chosen(d, t, dec.fused ? 1 : dec.gamma);
-        int32_t ctx = RQ(r_prompt, i) + RQ(r_tokens, i);
-        (void)ctx;
+        int32_t t = R[i].target;
+        if (d >= 0 && t >= 0 && ps) L.at(W.p_gprev, W.c.np, pair_of(d, t)) = dec.fused ? 1 : dec.gamma;
         if (dec.fused) {
             set_flag(i, kFused, true);
             record_gamma(i, 0);
-            push_item(t, 2 * i + 1, kOpDecode, 1, false);
+            enqueue(t, i, 1, kOpDecode, 1, false);
         } else {
             set_flag(i, kFused, false);
             record_gamma(i, dec.gamma);
-            RQ(r_pgamma, i) = dec.gamma;
+            R[i].pgamma = dec.gamma;
             set_phase(i, kPhSpeculating);
-            push_item(T + d, 2 * i + 1, kOpDecode, dec.gamma, false);
+            enqueue(T + d, i, 1, kOpDecode, dec.gamma, false);
         }
     }
 
     // finish_request (engine.cpp:449-468) + MetricsCollector::add_record
     DSD_HD void finish_request(int64_t i) {
-        RQ(r_done, i) = now;
-        if (RQ(r_first, i) < 0) RQ(r_first, i) = now;
+        ReqRec& r = R[i];
+        r.done = now;
+        if (r.first < 0) r.first = now;
         set_phase(i, kPhDone);
-        int32_t t = RQ(r_target, i);
+        const int32_t t = r.target;
         --SV(v_open, t);
-        int32_t out = RQ(r_output, i);
-        if (out >= 2 && S.pair_stats) {
-            double tpot = (static_cast<double>(now - RQ(r_first, i)) / 1000.0) /
-                          static_cast<double>(out - 1);
+        if (r.output >= 2 && ps) {
+            double tpot = (static_cast<double>(now - r.first) / 1000.0) / static_cast<double>(r.output - 1);
             push_tpot(t, tpot);
         }
         if (now > last_completion) last_completion = now;
@@ -655,26 +727,28 @@ struct Engine {
             int32_t v = T + d;
             if (SV(v_active, v) == static_cast<int32_t>(i)) {
                 SV(v_active, v) = -1;
-                activate_next_session(d);
+                push_act(act(kActActivate, static_cast<uint32_t>(d)));
             }
         }
     }
 
-    // commit_tokens (engine.cpp:437-447)
-    DSD_HD void commit_tokens(int64_t i, int32_t raw) {
-        int32_t remaining = RQ(r_output, i) - RQ(r_tokens, i);
+    // commit_tokens (engine.cpp:437-447); returns true when the request is done
+    DSD_HD bool commit_tokens(int64_t i, int32_t raw) {
+        ReqRec& r = R[i];
+        int32_t remaining = r.output - r.tokens;
         int32_t c = raw < remaining ? raw : remaining;
-        RQ(r_tokens, i) += c;
+        r.tokens += c;
         record_commit(i, c);
-        if (RQ(r_first, i) < 0) RQ(r_first, i) = now;
-        if (RQ(r_tokens, i) >= RQ(r_output, i)) finish_request(i);
+        if (r.first < 0) r.first = now;
+        return r.tokens >= r.output;
     }
 
     // consume_acceptance (engine.cpp:17-32) on the packed bits
     DSD_HD void consume_acceptance(int64_t i, int gamma, int& accepted, int& consumed) {
-        const uint64_t* bits = W.bits + rep * W.c.bw + RQ(r_bitoff, i);
-        const int32_t nb = RQ(r_nbits, i);
-        int32_t cur = RQ(r_cursor, i);
+        ReqRec& r = R[i];
+        const uint64_t* bits = W.bits + rep * W.c.bw + r.bitoff;
+        const int32_t nb = r.nbits;
+        int32_t cur = r.cursor;
         accepted = 0;
         consumed = 0;
         while (consumed < gamma) {
@@ -687,90 +761,54 @@ struct Engine {
                 break;
             }
         }
-        RQ(r_cursor, i) = cur;
+        r.cursor = cur;
     }
 
-    DSD_HD void send_proposal(int64_t i) {  // engine.cpp:591-597
-        set_phase(i, kPhInFlightToTarget);
-        int64_t dl = net_delay(RQ(r_drafter, i), RQ(r_target, i));
-        RQ(r_outd, i) = dl;
-        schedule(now + dl, info(kEvNetArrive, kMsgProposal, static_cast<uint32_t>(i)));
-    }
-
-    // on_target_item_done (engine.cpp:599-646)
-    DSD_HD void on_target_item_done(int64_t i, uint32_t op, int32_t tokens) {
+    // one member of a finished batch (engine.cpp:573-587, 591-646)
+    DSD_HD void item_done(int32_t slot) {
+        const int64_t i = slot >> 1;
+        const int k = slot & 1;
+        ReqRec& r = R[i];
+        const int32_t nxt = r.next[k];
+        const uint32_t op = r.op[k] & 3u;
+        if (nxt >= 0) push_act(act(kActItem, static_cast<uint32_t>(nxt)));
+        if (item_server >= T) {  // draft server
+            if (op == kOpPrefill) {
+                set_flag(i, kDpd, true);
+                if (r.output > 0) schedule(now, info(kEvIterStart, 0, static_cast<uint32_t>(i)));
+            } else {  // send_proposal (engine.cpp:591-597)
+                set_phase(i, kPhInFlightToTarget);
+                int64_t dl = net_delay(r.drafter, r.target);
+                r.outd = static_cast<int32_t>(dl);
+                schedule(now + dl, info(kEvNetArrive, kMsgProposal, static_cast<uint32_t>(i)));
+            }
+            return;
+        }
         if (op == kOpPrefill) {
             set_flag(i, kTpd, true);
-            if (RQ(r_output, i) == 0) {
-                if (phase(i) != kPhDone) finish_request(i);
-                return;
+            if (r.output == 0) {
+                if (phase(i) != kPhDone) push_act(act(kActFinish, static_cast<uint32_t>(i)));
+            } else if (flag(i, kFused) && fe) {
+                push_act(act(kActBegin, static_cast<uint32_t>(i) * 2));
             }
-            if (flag(i, kFused) && S.fused_everything) begin_iteration(i, Decision{true, 1});
         } else if (op == kOpVerify) {
             int acc, cons;
-            consume_acceptance(i, tokens, acc, cons);
-            RQ(r_lcr, i) = acc + 1;
-            RQ(r_prop, i) += cons;
-            RQ(r_acc, i) += acc;
-            int32_t d = RQ(r_drafter, i), t = RQ(r_target, i);
-            on_verify(d, t, cons, acc);
-            int64_t bd = net_delay(d, t);
-            RQ(r_backd, i) = bd;
+            consume_acceptance(i, r.tok1, acc, cons);
+            r.lcr = acc + 1;
+            r.prop += cons;
+            r.acc += acc;
+            on_verify(r.drafter, r.target, cons, acc);
+            int64_t bd = net_delay(r.drafter, r.target);
+            r.backd = static_cast<int32_t>(bd);
             set_phase(i, kPhInFlightToDraft);
             schedule(now + bd, info(kEvNetArrive, kMsgResult, static_cast<uint32_t>(i)));
-        } else {
-            commit_tokens(i, 1);
-            if (phase(i) == kPhDone) return;
-            if (S.fused_everything || draft_of(i) < 0) {
-                begin_iteration(i, Decision{true, 1});
+        } else {  // fused decode step: commit one token, then the next iteration
+            if (commit_tokens(i, 1)) {
+                push_act(act(kActFinish, static_cast<uint32_t>(i)));
             } else {
-                begin_iteration(i, decide_window(i));
+                const bool decide = !(fe || draft_of(i) < 0);
+                push_act(act(kActBegin, static_cast<uint32_t>(i) * 2 + (decide ? 1u : 0u)));
             }
-        }
-    }
-
-    // on_compute_done (engine.cpp:569-589)
-    DSD_HD void on_compute_done(int32_t v) {
-        SV(v_busy, v) = 0;
-        int32_t cur = SV(v_run, v);
-        SV(v_run, v) = -1;
-        const bool is_draft = v >= T;
-        while (cur >= 0) {
-            int32_t nxt = SL(s_next, cur);
-            uint32_t op = SL(s_op, cur) & 3u;
-            int32_t tok = SL(s_tok, cur);
-            int64_t i = cur >> 1;
-            if (is_draft) {
-                if (op == kOpPrefill) {
-                    set_flag(i, kDpd, true);
-                    if (RQ(r_output, i) > 0)
-                        schedule(now, info(kEvIterStart, 0, static_cast<uint32_t>(i)));
-                } else {
-                    send_proposal(i);
-                }
-            } else {
-                on_target_item_done(i, op, tok);
-            }
-            cur = nxt;
-        }
-        try_dispatch(v, false);
-    }
-
-    // on_net_arrive (engine.cpp:406-435)
-    DSD_HD void on_net_arrive(uint32_t msg, int64_t i) {
-        int32_t t = RQ(r_target, i);
-        if (msg == kMsgPrompt) {
-            push_item(t, 2 * i, kOpPrefill, RQ(r_prompt, i), true);
-        } else if (msg == kMsgProposal) {
-            set_phase(i, kPhVerifying);
-            push_item(t, 2 * i + 1, kOpVerify, RQ(r_pgamma, i), true);
-        } else {
-            if (S.pair_stats) {
-                on_rtt_sample(RQ(r_drafter, i), t,
-                              static_cast<double>(RQ(r_outd, i) + RQ(r_backd, i)) / 1000.0);
-            }
-            commit_tokens(i, RQ(r_lcr, i));
-            if (phase(i) != kPhDone) schedule(now, info(kEvIterStart, 0, static_cast<uint32_t>(i)));
         }
     }
 
@@ -782,23 +820,6 @@ struct Engine {
         N = (S.workload == 0) ? S.n_requests : S.tr_n;
         seq_next = static_cast<uint32_t>(N);
         if (W.collect) seqbase = W.rep_seqbase[rep];
-        for (int64_t i = 0; i < N; ++i) {
-            RQ(r_flags, i) = 0;
-            RQ(r_target, i) = -1;
-            RQ(r_tokens, i) = 0;
-            RQ(r_cursor, i) = 0;
-            RQ(r_first, i) = -1;
-            RQ(r_done, i) = -1;
-            RQ(r_pgamma, i) = 0;
-            RQ(r_lcr, i) = 0;
-            RQ(r_outd, i) = 0;
-            RQ(r_backd, i) = 0;
-            RQ(r_prop, i) = 0;
-            RQ(r_acc, i) = 0;
-            RQ(r_ng, i) = 0;
-            RQ(r_nc, i) = 0;
-            RQ(r_snext, i) = -1;
-        }
         for (int32_t v = 0; v < T + D; ++v) {
             SV(v_qhead, v) = -1;
             SV(v_qtail, v) = -1;
@@ -806,13 +827,13 @@ struct Engine {
             SV(v_busy, v) = 0;
             SV(v_armed, v) = 0;
             SV(v_armseq, v) = 0;
-            SV(v_busy_us, v) = 0;
+            busy_us(v) = 0;
             SV(v_active, v) = -1;
             SV(v_shead, v) = -1;
             SV(v_stail, v) = -1;
             SV(v_open, v) = 0;
         }
-        if (S.pair_stats) {
+        if (ps) {
             for (int32_t t = 0; t < T; ++t) {
                 L.at(W.t_tcnt, W.c.nt, t) = 0;
                 L.at(W.t_tpos, W.c.nt, t) = 0;
@@ -838,56 +859,118 @@ struct Engine {
         return k;
     }
 
-    DSD_HD void run() {
-        init();
-        for (;;) {
-            if (fail) break;
-            const bool have_arr = next_arr < N;
-            int64_t ai = 0, ta = 0;
-            if (have_arr) {
-                ai = arrival_index(next_arr);
-                ta = RQ(r_arrival, ai);
-            }
-            if (heap_n == 0 && !have_arr) break;
-            // arrivals hold seq 0..N-1: they win every time tie
-            if (have_arr && (heap_n == 0 || ta <= L.at(W.h_time, W.c.hc, 0))) {
-                ++next_arr;
-                now = ta;
-                ++processed;
-                on_arrival(ai);
-                continue;
-            }
-            const int64_t t = L.at(W.h_time, W.c.hc, 0);
-            const uint64_t key = L.at(W.h_key, W.c.hc, 0);
-            heap_pop();
-            now = t;
+    // Kind of this replica's next step: the top action, else kActPop while
+    // events remain, else kActNone.  The kernel's warp scheduler reads it.
+    DSD_HD uint32_t next_kind() const {
+        if (fail) return kActNone;
+        if (sp > 0) return st0 & 15u;
+        return (next_arr < N || heap_n > 0) ? static_cast<uint32_t>(kActPop) : static_cast<uint32_t>(kActNone);
+    }
+
+    // SimKernel::run_until's pop (event_queue.cpp:28-42): a 2-way merge of the
+    // arrival stream (seq 0..N-1, wins every time tie) with the dynamic heap.
+    // The event's handler becomes the next action.
+    DSD_HD void pop_event() {
+        const bool have_arr = next_arr < N;
+        int64_t ai = 0, ta = 0;
+        if (have_arr) {
+            ai = arrival_index(next_arr);
+            ta = R[ai].arrival;
+        }
+        if (have_arr && (heap_n == 0 || ta <= ht(0))) {
+            ++next_arr;
+            now = ta;
             ++processed;
-            const uint32_t inf = static_cast<uint32_t>(key);
-            const uint32_t kind = inf & 7u;
-            const uint32_t msg = (inf >> 3) & 3u;
-            const uint32_t id = inf >> 5;
-            switch (kind) {
-                case kEvIterStart:
-                    begin_iteration(id, decide_window(id));
-                    break;
-                case kEvNetArrive:
-                    on_net_arrive(msg, id);
-                    break;
-                case kEvComputeDone:
-                    on_compute_done(static_cast<int32_t>(id));
-                    break;
-                case kEvBatchReady: {
-                    int32_t v = static_cast<int32_t>(id);
-                    if (SV(v_armed, v) && SV(v_armseq, v) == static_cast<uint32_t>(key >> 32)) {
-                        SV(v_armed, v) = 0;
-                        try_dispatch(v, true);
-                    }
-                    break;
-                }
-                default:
-                    break;
+            push_act(act(kActArrival, static_cast<uint32_t>(ai)));
+            return;
+        }
+        const int64_t t = ht(0);
+        const uint64_t key = hk(0);
+        heap_pop();
+        now = t;
+        ++processed;
+        const uint32_t inf = static_cast<uint32_t>(key);
+        const uint32_t kind = inf & 7u;
+        const uint32_t msg = (inf >> 3) & 3u;
+        const uint32_t id = inf >> 5;
+        if (kind == kEvIterStart) {
+            push_act(act(kActBegin, id * 2 + 1));
+        } else if (kind == kEvNetArrive) {
+            push_act(act(kActNetPrompt + msg, id));
+        } else if (kind == kEvComputeDone) {
+            push_act(act(kActComputeDone, id));
+        } else if (kind == kEvBatchReady) {  // engine.cpp:265-271
+            const int32_t v = static_cast<int32_t>(id);
+            if (SV(v_armed, v) && SV(v_armseq, v) == static_cast<uint32_t>(key >> 32)) {
+                SV(v_armed, v) = 0;
+                push_act(act(kActDispatch, static_cast<uint32_t>(v) * 2 + 1));
             }
         }
+    }
+
+    // Executes exactly one step of kind next_kind().
+    DSD_HD void step() {
+        if (sp == 0) {
+            pop_event();
+            return;
+        }
+        const uint32_t a = pop_act();
+        const uint32_t arg = a >> 4;
+        switch (a & 15u) {
+            case kActDispatch: try_dispatch(static_cast<int32_t>(arg >> 1), arg & 1u); break;
+            case kActActivate: activate_next_session(static_cast<int32_t>(arg)); break;
+            case kActItem: item_done(static_cast<int32_t>(arg)); break;
+            case kActBegin: begin(arg >> 1, arg & 1u); break;
+            case kActFinish: finish_request(arg); break;
+            case kActSendPrompt: {
+                ReqRec& r = R[arg];
+                int64_t delay = net_delay(r.drafter, r.target);
+                schedule(now + delay, info(kEvNetArrive, kMsgPrompt, arg));
+                break;
+            }
+            case kActArrival: on_arrival(arg); break;
+            case kActNetPrompt: {  // on_net_arrive (engine.cpp:406-435)
+                ReqRec& r = R[arg];
+                enqueue(r.target, arg, 0, kOpPrefill, r.prompt, true);
+                break;
+            }
+            case kActNetProposal: {
+                ReqRec& r = R[arg];
+                set_phase(arg, kPhVerifying);
+                enqueue(r.target, arg, 1, kOpVerify, r.pgamma, true);
+                break;
+            }
+            case kActNetResult: {  // on_result_at_draft (engine.cpp:428-435)
+                ReqRec& r = R[arg];
+                if (ps)
+                    on_rtt_sample(r.drafter, r.target, static_cast<double>(static_cast<int64_t>(r.outd) + r.backd) / 1000.0);
+                if (commit_tokens(arg, r.lcr)) {
+                    push_act(act(kActFinish, arg));
+                } else {
+                    schedule(now, info(kEvIterStart, 0, arg));
+                }
+                break;
+            }
+            default: {  // kActComputeDone: on_compute_done (engine.cpp:569-589)
+                const int32_t v = static_cast<int32_t>(arg);
+                SV(v_busy, v) = 0;
+                const int32_t head = SV(v_run, v);
+                SV(v_run, v) = -1;
+                push_act(act(kActDispatch, static_cast<uint32_t>(v) * 2));
+                if (head >= 0) {
+                    item_server = v;
+                    push_act(act(kActItem, static_cast<uint32_t>(head)));
+                }
+                break;
+            }
+        }
+    }
+
+    // Single-replica driver (host debug builds); the kernel interleaves the
+    // steps of a warp's replicas with the warp scheduler instead.
+    DSD_HD void run() {
+        init();
+        while (next_kind() != kActNone) step();
         finish();
     }
 
@@ -911,14 +994,12 @@ struct Engine {
         double ttft = 0.0, tpot = 0.0;
         int64_t n_tpot = 0, n_rec = 0;
         for (int64_t i = 0; i < N; ++i) {  // records sorted by request id
-            int64_t done = RQ(r_done, i);
-            if (done < 0) continue;
+            const ReqRec& r = R[i];
+            if (r.done < 0) continue;
             ++n_rec;
-            int64_t first = RQ(r_first, i);
-            ttft += static_cast<double>(first - RQ(r_arrival, i)) / 1000.0;
-            int32_t out = RQ(r_output, i);
-            if (out >= 2) {
-                tpot += (static_cast<double>(done - first) / 1000.0) / static_cast<double>(out - 1);
+            ttft += static_cast<double>(r.first - r.arrival) / 1000.0;
+            if (r.output >= 2) {
+                tpot += (static_cast<double>(r.done - r.first) / 1000.0) / static_cast<double>(r.output - 1);
                 ++n_tpot;
             }
         }
@@ -928,22 +1009,52 @@ struct Engine {
         W.summary[rep] = s;
         W.fail[rep] = fail;
     }
-#undef RQ
-#undef SL
 #undef SV
 };
 
 // ---------------------------------------------------------------------------
 // workload staging: generate_synthetic (trace.cpp:145-187), trace copy, and the
-// engine's poisson re-sampling (engine.cpp:224-238).  One thread per replica.
+// engine's poisson re-sampling (engine.cpp:224-238).  One thread per replica;
+// writes each request's complete initial record.
 // ---------------------------------------------------------------------------
+DSD_HD void init_record(ReqRec& r, int64_t arrival, int32_t prompt, int32_t output, int32_t drafter,
+                        int32_t bitoff, int32_t nbits, int32_t seqoff) {
+    r.arrival = arrival;
+    r.first = -1;
+    r.done = -1;
+    r.enq[0] = 0;
+    r.enq[1] = 0;
+    r.prompt = prompt;
+    r.output = output;
+    r.drafter = drafter;
+    r.target = -1;
+    r.bitoff = bitoff;
+    r.nbits = nbits;
+    r.tokens = 0;
+    r.cursor = 0;
+    r.pgamma = 0;
+    r.lcr = 0;
+    r.outd = 0;
+    r.backd = 0;
+    r.prop = 0;
+    r.acc = 0;
+    r.ng = 0;
+    r.nc = 0;
+    r.snext = -1;
+    r.seqoff = seqoff;
+    r.next[0] = -1;
+    r.next[1] = -1;
+    r.tok1 = 0;
+    r.flags = 0;
+    r.op[0] = 0;
+    r.op[1] = 0;
+    r.pad = 0;
+}
+
 DSD_HD void stage_workload(const Workspace& W, int64_t rep) {
     const DevScenario& S = W.scen[W.rep_scen[rep]];
     const char* blob = W.blob;
-    Lane L;
-    L.w = rep / kLanes;
-    L.lane = static_cast<int>(rep % kLanes);
-    const int64_t nr = W.c.nr;
+    ReqRec* R = W.req + rep * W.c.nr;
     uint64_t* bits = W.bits + rep * W.c.bw;
     int64_t word = 0;
     int64_t lsum = 0;
@@ -958,18 +1069,14 @@ DSD_HD void stage_workload(const Workspace& W, int64_t rep) {
         const double alpha = S.alpha;
         for (int64_t n = 0; n < S.n_requests; ++n) {
             clock_ms += arrivals.exponential(S.mean_gap_ms);
-            L.at(W.r_arrival, nr, n) = llround(clock_ms * 1000.0);
+            const int64_t arr = llround(clock_ms * 1000.0);
             int64_t p = llround(lengths.lognormal(S.p_mu, S.p_sigma));
             p = p < 1 ? 1 : (S.p_cap < p ? S.p_cap : p);
             int64_t o = llround(lengths.lognormal(S.o_mu, S.o_sigma));
             o = o < 1 ? 1 : (S.o_cap < o ? S.o_cap : o);
-            L.at(W.r_prompt, nr, n) = static_cast<int32_t>(p);
-            L.at(W.r_output, nr, n) = static_cast<int32_t>(o);
-            L.at(W.r_drafter, nr, n) =
-                static_cast<int32_t>(drafter.below(static_cast<uint64_t>(S.gen_n_drafts)));
-            L.at(W.r_bitoff, nr, n) = static_cast<int32_t>(word);
-            L.at(W.r_nbits, nr, n) = static_cast<int32_t>(o);
-            L.at(W.r_seqoff, nr, n) = lsum;
+            const int32_t dr = static_cast<int32_t>(drafter.below(static_cast<uint64_t>(S.gen_n_drafts)));
+            init_record(R[n], arr, static_cast<int32_t>(p), static_cast<int32_t>(o), dr, static_cast<int32_t>(word),
+                        static_cast<int32_t>(o), static_cast<int32_t>(lsum));
             lsum += o;
             for (int64_t k = 0; k < o; k += 64) {
                 int64_t m = o - k < 64 ? o - k : 64;
@@ -992,25 +1099,22 @@ DSD_HD void stage_workload(const Workspace& W, int64_t rep) {
         arrivals.seed(W.rep_seed[rep], kLabelArrivals);
         double clock_ms = 0.0;
         for (int64_t n = 0; n < S.tr_n; ++n) {
+            int64_t arr;
             if (S.workload == 2) {
                 clock_ms += arrivals.exponential(1000.0 / S.rate_rps);
-                L.at(W.r_arrival, nr, n) = llround(clock_ms * 1000.0);
+                arr = llround(clock_ms * 1000.0);
             } else {
-                L.at(W.r_arrival, nr, n) = ta[n];
+                arr = ta[n];
             }
-            L.at(W.r_prompt, nr, n) = static_cast<int32_t>(tp[n]);
-            L.at(W.r_output, nr, n) = static_cast<int32_t>(to[n]);
-            L.at(W.r_drafter, nr, n) = static_cast<int32_t>(td[n]);
-            L.at(W.r_bitoff, nr, n) = static_cast<int32_t>(word);
             const int64_t nb = tb[n + 1] - tb[n];
-            L.at(W.r_nbits, nr, n) = static_cast<int32_t>(nb);
-            L.at(W.r_seqoff, nr, n) = lsum;
+            init_record(R[n], arr, static_cast<int32_t>(tp[n]), static_cast<int32_t>(to[n]),
+                        static_cast<int32_t>(td[n]), static_cast<int32_t>(word), static_cast<int32_t>(nb),
+                        static_cast<int32_t>(lsum));
             lsum += to[n];
             for (int64_t k = 0; k < nb; k += 64) {
                 int64_t m = nb - k < 64 ? nb - k : 64;
                 uint64_t acc = 0;
-                for (int64_t j = 0; j < m; ++j)
-                    acc |= static_cast<uint64_t>(tbits[tb[n] + k + j] & 1u) << j;
+                for (int64_t j = 0; j < m; ++j) acc |= static_cast<uint64_t>(tbits[tb[n] + k + j] & 1u) << j;
                 bits[word++] = acc;
             }
         }

@@ -16,6 +16,13 @@ namespace dsd {
 
 constexpr int kLanes = 32;
 constexpr int kMaxHidden = 64;  // AWC hidden width supported by the engine
+constexpr int kServerFields = 10;
+// Shared-memory variant of the simulation kernel: per-warp server state and a
+// heap of kSmemHeap slots live in shared memory; a replica whose dynamic event
+// heap outgrows it is re-run on the HBM variant.
+constexpr int kSmemServers = 4;
+constexpr int kSmemHeap = 24;
+constexpr int kSmemWarpBytes = kServerFields * kSmemServers * kLanes * 4 + kSmemHeap * kLanes * 16;
 
 // Event kinds (proj/include/specsim/sim/event_queue.hpp:12-18).
 enum : uint32_t { kEvArrival = 0, kEvBatchReady = 1, kEvComputeDone = 2, kEvNetArrive = 3, kEvIterStart = 4 };
@@ -30,12 +37,24 @@ enum : uint32_t {
 };
 
 // Per-replica failure codes (summary.status carries DSD_ERR_RUNTIME, detail here).
-enum : int32_t { kFailNone = 0, kFailHeap = 1, kFailAwcDims = 2, kFailSeq = 3 };
+enum : int32_t { kFailNone = 0, kFailHeap = 1, kFailAwcDims = 2, kFailSeq = 3, kFailStack = 4 };
+
+// Segment of a clamped integer query on one grid axis: the bracketing
+// indices and the interpolation weight, exactly as Grid::interpolate computes
+// them (profile.cpp:57-88).  Latency queries are integers (batch size,
+// batch*tokens, prompt or context tokens), so each axis gets a table indexed
+// by the query, built on the host with the same formula.
+struct AxisSeg {
+    int32_t lo, hi;
+    double t;
+};
 
 struct DevGrid {
     int32_t nb, nc;
     int64_t o_batch, o_ctx, o_vals;  // byte offsets into the blob (double arrays)
     double calibration;
+    int64_t o_btab, o_ctab;          // AxisSeg tables (-1: query by binary search)
+    int32_t nbt, nct;                // table sizes; queries >= size use the last entry
 };
 
 // A resolved scenario (dsd_scenario) in device form.  Offsets are bytes into
@@ -92,6 +111,34 @@ struct DevRecord {  // == dsd_request_record
     int32_t target_id, n_iterations;
 };
 
+// Everything the engine keeps about one request (RequestState, engine.cpp:86-106,
+// plus its two work-item slots) in a single 128-byte line, so the handful of
+// fields an event touches cost one L1 line instead of one line per field.
+// Work-item slot k of request i has id 2*i + k: k = 0 is the target prefill
+// item, k = 1 is the request's other item (draft prefill / draft decode /
+// verify / fused decode); a request never has two items of the same slot.
+struct alignas(128) ReqRec {
+    int64_t arrival;       // arrival event time (trace or re-sampled)
+    int64_t first;         // first-token time, -1 before the first commit
+    int64_t done;          // completion time, -1 while running
+    int64_t enq[2];        // enqueue time of slot 0 / 1
+    int32_t prompt, output;
+    int32_t drafter, target;
+    int32_t bitoff, nbits;  // packed acceptance bits: word offset, length
+    int32_t tokens, cursor;  // tokens_done, accept cursor (mod nbits)
+    int32_t pgamma, lcr;     // pending gamma, last committed raw
+    int32_t outd, backd;     // the two legs of the last exchange (us)
+    int32_t prop, acc;       // proposed_total, accepted_total
+    int32_t ng, nc;          // gamma_sequence / committed_sequence lengths
+    int32_t snext, seqoff;   // draft session FIFO link, sequence-arena offset
+    int32_t next[2];         // work-queue / running-batch links of slot 0 / 1
+    int32_t tok1;            // tokens of slot 1 (slot 0 always carries the prompt)
+    uint8_t flags;           // phase | dpd<<3 | tpd<<4 | fused<<5
+    uint8_t op[2];           // op | via_network<<2 of slot 0 / 1
+    uint8_t pad;
+};
+static_assert(sizeof(ReqRec) == 128, "request record must be one 128-byte line");
+
 struct Workspace {
     Caps c;
     const char* blob;
@@ -101,46 +148,14 @@ struct Workspace {
     const uint64_t* rep_gen_seed;
     DevSummary* summary;  // [n]
     int32_t* fail;        // [n]
-    // ---- per request (cap nr, interleaved) ----
-    int32_t* r_prompt;
-    int32_t* r_output;
-    int64_t* r_arrival;
-    int32_t* r_drafter;
-    int32_t* r_bitoff;   // word offset into the replica's bit region
-    int32_t* r_nbits;    // acceptance sequence length
-    uint8_t* r_flags;    // phase | dpd<<3 | tpd<<4 | fused<<5
-    int32_t* r_target;
-    int32_t* r_tokens;
-    int32_t* r_cursor;   // accept cursor modulo nbits
-    int64_t* r_first;
-    int64_t* r_done;     // completion time, -1 while running
-    int32_t* r_pgamma;
-    int32_t* r_lcr;      // last committed raw
-    int64_t* r_outd;
-    int64_t* r_backd;
-    int32_t* r_prop;
-    int32_t* r_acc;
-    int32_t* r_ng;       // gamma_sequence length
-    int32_t* r_nc;       // committed_sequence length
-    int32_t* r_snext;    // draft session FIFO link
-    int64_t* r_seqoff;   // offset of the request's sequences in the seq arena (records only)
-    // ---- work-item slots (cap 2*nr, interleaved): slot 2i = target prefill, 2i+1 = other ----
-    uint8_t* s_op;       // op | via_network<<2
-    int32_t* s_tok;
-    int64_t* s_enq;
-    int32_t* s_next;
+    // ---- per request: one 128-byte record, replica-contiguous [n][nr] ----
+    ReqRec* req;
     // ---- per server (cap ns, interleaved): targets 0..T-1, drafts T.. ----
-    int32_t* v_qhead;
-    int32_t* v_qtail;
-    int32_t* v_run;
-    uint8_t* v_busy;
-    uint8_t* v_armed;
-    uint32_t* v_armseq;
+    // kServerFields int32 fields x ns servers per warp block (queue head/tail,
+    // running batch, busy, armed, armed-event seq, active session, session
+    // FIFO head/tail, open requests); used when the batch runs the HBM variant
+    int32_t* srv;
     int64_t* v_busy_us;
-    int32_t* v_active;
-    int32_t* v_shead;
-    int32_t* v_stail;
-    int32_t* v_open;
     // ---- per target TPOT ring (cap nt*50) and per pair stats (cap np) ----
     double* t_tpot;
     int32_t* t_tpos;     // cap nt
@@ -163,6 +178,9 @@ struct Workspace {
     uint64_t* h_key;     // seq<<32 | info
     // ---- acceptance bits: replica-contiguous [n][bw] ----
     uint64_t* bits;
+    // ---- optional step profile (DSD_STEP_STATS=1): [2k] cycles, [2k+1] count
+    // per step kind, [32] warp iterations, [33] warp cycles, [34] max iterations
+    unsigned long long* step_stats;
     // ---- records (optional) ----
     int32_t collect;
     int64_t* rep_seqbase;  // [n] offset into the sequence arena

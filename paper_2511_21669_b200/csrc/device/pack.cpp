@@ -40,6 +40,34 @@ int64_t awc_param_count(const dsd_awc_model& m) {
     return H * I + H + static_cast<int64_t>(m.blocks) * (2 * H * H + 2 * H) + H + 1;
 }
 
+// Segment table of one axis for integer queries 0..Q, Q = ceil(axis.back())
+// (larger queries clamp to the same entry).  Each entry is what
+// Grid::interpolate computes for that query (profile.cpp:20-27, 64-84):
+// clamp, upper_bound segment, weight (q - a[lo]) / (a[hi] - a[lo]).
+int64_t axis_table(BlobBuilder& B, const double* axis, int n, int32_t* size) {
+    const double back = axis[n - 1];
+    if (!(back >= 0.0) || back > 65536.0) {
+        *size = 0;
+        return -1;
+    }
+    const int32_t q_max = static_cast<int32_t>(std::ceil(back));
+    std::vector<AxisSeg> tab(static_cast<size_t>(q_max) + 1);
+    for (int32_t q = 0; q <= q_max; ++q) {
+        double v = static_cast<double>(q);
+        if (v < axis[0]) v = axis[0];
+        else if (v > back) v = back;
+        int lo = 0;
+        if (n > 1) {
+            int hi = static_cast<int>(std::upper_bound(axis, axis + n, v) - axis);
+            lo = hi == 0 ? 0 : (hi >= n ? n - 2 : hi - 1);
+        }
+        const int hi = std::min(lo + 1, n - 1);
+        tab[static_cast<size_t>(q)] = AxisSeg{lo, hi, hi == lo ? 0.0 : (v - axis[lo]) / (axis[hi] - axis[lo])};
+    }
+    *size = q_max + 1;
+    return B.put(tab.data(), sizeof(AxisSeg) * tab.size(), false);
+}
+
 }  // namespace
 
 Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n) {
@@ -86,6 +114,9 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
                     cfg_error("link rtt_ms/jitter_ms must be >= 0");
                 if (s.links[l].jitter_ms > s.links[l].rtt_ms)
                     cfg_error("link jitter_ms must not exceed rtt_ms");
+                // one-way delays are held as int32 microseconds on the device
+                if (!(s.links[l].rtt_ms <= 2.0e6))
+                    throw Error(DSD_ERR_RUNTIME, "link rtt_ms above the engine limit of 2e6 ms");
             }
             d.o_links = B.put(s.links, sizeof(dsd_link) * (s.n_drafts > 0 ? nl : 1));
         }
@@ -111,6 +142,8 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
                 g[gi].o_vals =
                     B.put(src.values_ms, sizeof(double) * src.n_batch * src.n_context);
                 g[gi].calibration = src.calibration;
+                g[gi].o_btab = axis_table(B, src.batch_axis, src.n_batch, &g[gi].nbt);
+                g[gi].o_ctab = axis_table(B, src.context_axis, src.n_context, &g[gi].nct);
             }
             int64_t off = B.put(g.data(), sizeof(DevGrid) * g.size(), false);
             git = grid_tables.emplace(s.grids, off).first;
@@ -182,7 +215,7 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
         if (d.pair_stats) any_pairs = true;
         // workload
         d.workload = s.workload;
-        int64_t N = 0, bw = 0;
+        int64_t N = 0, bw = 0, lbound = 0;
         if (s.workload == DSD_WORKLOAD_SYNTHETIC) {
             // generate_synthetic preconditions (trace.cpp:146-153)
             if (!(s.acceptance_rate >= 0.0 && s.acceptance_rate <= 1.0))
@@ -207,6 +240,7 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
             d.gen_n_drafts = s.gen_n_drafts;
             N = s.n_requests;
             bw = N * ((s.output_cap + 63) / 64);
+            lbound = N * s.output_cap;
         } else if (s.workload == DSD_WORKLOAD_TRACE || s.workload == DSD_WORKLOAD_TRACE_POISSON) {
             if (!s.trace) cfg_error("trace workload without a trace");
             const dsd_trace& t = *s.trace;
@@ -232,6 +266,7 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
                 if (t.prompt_length[i] > INT32_MAX || t.output_length[i] > INT32_MAX)
                     cfg_error(rw + "length exceeds engine limits");
                 bw += (nb + 63) / 64;
+                lbound += t.output_length[i];
                 if (i > 0 && t.arrival_us[i] < t.arrival_us[i - 1]) sorted = false;
             }
             d.tr_n = N;
@@ -252,7 +287,9 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
         } else {
             cfg_error("unknown workload kind");
         }
-        if (N >= (int64_t(1) << 26)) cfg_error("too many requests per replica");
+        if (N >= (int64_t(1) << 26)) throw Error(DSD_ERR_RUNTIME, "too many requests per replica (engine limit 2^26)");
+        if (lbound >= (int64_t(1) << 31) || bw >= (int64_t(1) << 31))
+            throw Error(DSD_ERR_RUNTIME, "total output tokens per replica above the engine limit of 2^31");
         scen_nr[k] = N;
         scen_bw[k] = bw;
         c.nr = std::max(c.nr, N);
@@ -295,17 +332,11 @@ size_t layout_workspace(Workspace& W, const Caps& c, char* base) {
         using T = std::remove_reference_t<decltype(*ptr)>;
         fields.emplace_back(reinterpret_cast<void**>(&ptr), sizeof(T) * static_cast<size_t>(cap * lanes));
     };
-    field(W.r_prompt, c.nr); field(W.r_output, c.nr); field(W.r_arrival, c.nr);
-    field(W.r_drafter, c.nr); field(W.r_bitoff, c.nr); field(W.r_nbits, c.nr);
-    field(W.r_flags, c.nr); field(W.r_target, c.nr); field(W.r_tokens, c.nr);
-    field(W.r_cursor, c.nr); field(W.r_first, c.nr); field(W.r_done, c.nr);
-    field(W.r_pgamma, c.nr); field(W.r_lcr, c.nr); field(W.r_outd, c.nr);
-    field(W.r_backd, c.nr); field(W.r_prop, c.nr); field(W.r_acc, c.nr);
-    field(W.r_ng, c.nr); field(W.r_nc, c.nr); field(W.r_snext, c.nr); field(W.r_seqoff, c.nr);
-    field(W.s_op, 2 * c.nr); field(W.s_tok, 2 * c.nr); field(W.s_enq, 2 * c.nr); field(W.s_next, 2 * c.nr);
-    field(W.v_qhead, c.ns); field(W.v_qtail, c.ns); field(W.v_run, c.ns); field(W.v_busy, c.ns);
-    field(W.v_armed, c.ns); field(W.v_armseq, c.ns); field(W.v_busy_us, c.ns); field(W.v_active, c.ns);
-    field(W.v_shead, c.ns); field(W.v_stail, c.ns); field(W.v_open, c.ns);
+    // request records are replica-contiguous (not lane-interleaved): `lanes`
+    // replicas x nr records of 128 bytes
+    field(W.req, c.nr);
+    field(W.srv, kServerFields * c.ns);
+    field(W.v_busy_us, c.ns);
     if (c.np > 0) {
         field(W.t_tpot, c.nt * 50); field(W.t_tpos, c.nt); field(W.t_tcnt, c.nt);
         field(W.p_acc_ex, c.np * 20); field(W.p_acc_ac, c.np * 20); field(W.p_acc_pos, c.np);

@@ -9,8 +9,10 @@
 
 #ifdef __CUDACC__
 #define DSD_HD __host__ __device__ __forceinline__
+#define DSD_HD_NOINLINE __host__ __device__ __noinline__
 #else
 #define DSD_HD inline
+#define DSD_HD_NOINLINE
 #endif
 
 namespace dsd {

@@ -4,6 +4,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -31,23 +33,116 @@ constexpr int kBlock = 64;
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_stage(Workspace W, int64_t* ltot) {
-    int64_t rep = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (rep >= W.c.n) return;
+// Replica lists: the first launch covers replicas 0..n-1 (list == nullptr);
+// the overflow re-run covers the `*count` replicas in `list`.
+__device__ __forceinline__ bool replica_of(const Workspace& W, const int32_t* list, const int32_t* count,
+                                          int64_t t, int64_t& rep) {
+    if (list) {
+        if (t >= *count) return false;
+        rep = list[t];
+        return true;
+    }
+    rep = t;
+    return t < W.c.n;
+}
+
+__global__ void __launch_bounds__(kBlock) k_stage(Workspace W, int64_t* ltot, const int32_t* list,
+                                                  const int32_t* count) {
+    int64_t rep;
+    if (!replica_of(W, list, count, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x, rep)) return;
     stage_workload(W, rep);
     if (ltot) {
         const DevScenario& S = W.scen[W.rep_scen[rep]];
         int64_t N = S.workload == 0 ? S.n_requests : S.tr_n;
-        Lane L{rep / kLanes, static_cast<int>(rep % kLanes)};
-        ltot[rep] = N == 0 ? 0 : L.at(W.r_seqoff, W.c.nr, N - 1) + L.at(W.r_output, W.c.nr, N - 1);
+        const ReqRec* R = W.req + rep * W.c.nr;
+        ltot[rep] = N == 0 ? 0 : static_cast<int64_t>(R[N - 1].seqoff) + R[N - 1].output;
     }
 }
 
-__global__ void __launch_bounds__(kBlock) k_simulate(Workspace W) {
-    int64_t rep = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+// One thread per replica; each iteration the warp runs ONE kind of step, for
+// the lanes whose next step is of that kind.  Kinds are visited in a cyclic
+// sweep (one __reduce_or_sync finds the next kind any lane has pending), in
+// lifecycle order, so a lane typically advances through a whole event per
+// sweep and lanes fall into phase with each other.  Replicas are independent,
+// so reordering steps across lanes is free; the warp executes one handler
+// body per iteration instead of the union of all of them.
+//
+// kSmem: the warp's server state and the first `heap_cap` event-heap slots
+// live in shared memory (small topologies, <= kSmemServers servers); a replica
+// whose heap would outgrow them fails with kFailHeap and is re-run on the HBM
+// variant (k_collect_overflow + k_stage + k_simulate<false>).
+//
+// __launch_bounds__(64, 8): <= 128 registers, so 8 blocks (16 warps) fit per
+// SM and a 65,536-replica sweep (13.8 warps/SM on 148 SMs) is one wave.
+template <bool kSmem>
+__global__ void __launch_bounds__(kBlock, 8) k_simulate(Workspace W, const int32_t* list, const int32_t* count,
+                                                     int32_t smem_heap_cap) {
+    int64_t rep = 0;
+    const bool live = replica_of(W, list, count, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x, rep);
+    const int64_t r = live ? rep : 0;
+    int32_t* sbase;
+    int64_t* hb;
+    uint64_t* kb;
+    int64_t hcap;
+    int32_t nsc;
+    if constexpr (kSmem) {
+        extern __shared__ __align__(16) unsigned char smem[];
+        const int lane = threadIdx.x % kLanes;
+        nsc = static_cast<int32_t>(W.c.ns);
+        hcap = smem_heap_cap;
+        const int64_t srv_bytes = static_cast<int64_t>(kServerFields) * nsc * kLanes * 4;
+        unsigned char* blk = smem + (threadIdx.x / kLanes) * (srv_bytes + hcap * kLanes * 16);
+        sbase = reinterpret_cast<int32_t*>(blk) + lane;
+        hb = reinterpret_cast<int64_t*>(blk + srv_bytes) + lane;
+        kb = reinterpret_cast<uint64_t*>(blk + srv_bytes + hcap * kLanes * 8) + lane;
+    } else {
+        const int64_t w = r / kLanes, lane = r % kLanes;
+        nsc = static_cast<int32_t>(W.c.ns);
+        hcap = W.c.hc;
+        sbase = W.srv + w * kServerFields * W.c.ns * kLanes + lane;
+        hb = W.h_time + w * W.c.hc * kLanes + lane;
+        kb = W.h_key + w * W.c.hc * kLanes + lane;
+    }
+    Engine e(W, W.scen[W.rep_scen[r]], r, sbase, hb, kb, hcap, nsc);
+    if (live) e.init();
+    uint32_t kind = live ? e.next_kind() : static_cast<uint32_t>(kActNone);
+    uint32_t sweep = 0;  // next kind the warp considers
+    unsigned long long* stats = W.step_stats;  // optional per-kind cycle profile
+    long long t_start = stats ? clock64() : 0;
+    unsigned long long iters = 0;
+    for (;;) {
+        const unsigned present = __reduce_or_sync(0xffffffffu, kind == kActNone ? 0u : (1u << kind));
+        if (present == 0u) break;
+        const unsigned twice = present | (present << kActKinds);  // cyclic scan from `sweep`
+        const uint32_t pick = (sweep + __ffs(twice >> sweep) - 1) % kActKinds;
+        if (kind == pick) {
+            if (stats) {
+                const long long t0 = clock64();
+                e.step();
+                const long long t1 = clock64();
+                atomicAdd(&stats[2 * pick], static_cast<unsigned long long>(t1 - t0));
+                atomicAdd(&stats[2 * pick + 1], 1ull);
+            } else {
+                e.step();
+            }
+            kind = e.next_kind();
+        }
+        sweep = pick + 1 == kActKinds ? 0 : pick + 1;
+        ++iters;
+    }
+    if (stats && (threadIdx.x % kLanes) == 0) {
+        atomicAdd(&stats[32], iters);                                                    // warp iterations
+        atomicAdd(&stats[33], static_cast<unsigned long long>(clock64() - t_start));  // warp cycles
+        atomicMax(&stats[34], iters);
+    }
+    if (live) e.finish();
+}
+
+// Collects the replicas whose shared-memory heap overflowed.
+__global__ void k_collect_overflow(Workspace W, int32_t* list, int32_t* count) {
+    const int64_t rep = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (rep >= W.c.n) return;
-    Engine e(W, W.scen[W.rep_scen[rep]], rep);
-    e.run();
+    if (W.fail[rep] == kFailHeap) list[atomicAdd(count, 1)] = static_cast<int32_t>(rep);
 }
 
 __global__ void k_export(Workspace W, DevRecord* rec, int64_t* busy) {
@@ -57,18 +152,19 @@ __global__ void k_export(Workspace W, DevRecord* rec, int64_t* busy) {
     Lane L{rep / kLanes, static_cast<int>(rep % kLanes)};
     const int64_t nr = W.c.nr;
     int64_t N = S.workload == 0 ? S.n_requests : S.tr_n;
+    const ReqRec* R = W.req + rep * nr;
     for (int64_t i = 0; i < N; ++i) {
         DevRecord r;
-        r.drafter_id = S.n_drafts > 0 ? L.at(W.r_drafter, nr, i) : -1;
-        r.prompt_length = L.at(W.r_prompt, nr, i);
-        r.output_length = L.at(W.r_output, nr, i);
-        r.arrival_us = L.at(W.r_arrival, nr, i);
-        r.first_token_us = L.at(W.r_first, nr, i);
-        r.completion_us = L.at(W.r_done, nr, i);
-        r.proposed = L.at(W.r_prop, nr, i);
-        r.accepted = L.at(W.r_acc, nr, i);
-        r.target_id = L.at(W.r_target, nr, i);
-        r.n_iterations = L.at(W.r_ng, nr, i);
+        r.drafter_id = S.n_drafts > 0 ? R[i].drafter : -1;
+        r.prompt_length = R[i].prompt;
+        r.output_length = R[i].output;
+        r.arrival_us = R[i].arrival;
+        r.first_token_us = R[i].first;
+        r.completion_us = R[i].done;
+        r.proposed = R[i].prop;
+        r.accepted = R[i].acc;
+        r.target_id = R[i].target;
+        r.n_iterations = R[i].ng;
         rec[rep * nr + i] = r;
     }
     for (int32_t t = 0; t < S.n_targets; ++t) busy[rep * W.c.nt + t] = L.at(W.v_busy_us, W.c.ns, t);
@@ -98,7 +194,12 @@ struct RuntimeImpl {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[4] = {};
-    DevBuf blob, scen, reps, arena, summary, fail, ltot, seqbase, seqg, seqc, rec, busy;
+    DevBuf blob, scen, reps, arena, summary, fail, ltot, seqbase, seqg, seqc, rec, busy, ovf;
+    // shared-memory heap slots per replica for small topologies (0 = always
+    // run the HBM variant; env DSD_SMEM_HEAP overrides, for tests)
+    int32_t smem_heap = 8;
+    bool step_stats = false;  // env DSD_STEP_STATS=1: per-step-kind cycle profile to stderr
+    DevBuf stats;
     Workspace W{};
     std::vector<DevScenario> host_scen;
     std::vector<int64_t> host_seqbase;
@@ -108,6 +209,7 @@ struct RuntimeImpl {
     bool prepared = false;
     bool ran = false;
     int64_t launches = 0;
+    int64_t h2d_bytes = 0, d2h_bytes = 0;
     // records cache (filled lazily after a collect run)
     bool rec_cached = false;
     std::vector<DevRecord> h_rec;
@@ -128,6 +230,8 @@ Runtime::Runtime(int device) : impl_(new RuntimeImpl) {
     if (prop.major < 10)
         throw Error(DSD_ERR_RUNTIME, std::string("device ") + prop.name + " is not sm_100-class");
     DSD_CUDA(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking));
+    if (const char* h = std::getenv("DSD_SMEM_HEAP")) impl_->smem_heap = std::max(0, std::atoi(h));
+    if (const char* s = std::getenv("DSD_STEP_STATS")) impl_->step_stats = std::atoi(s) != 0;
     for (auto& ev : impl_->ev) DSD_CUDA(cudaEventCreate(&ev));
 }
 
@@ -143,6 +247,10 @@ Runtime::~Runtime() {
 void* Runtime::stream() { return impl_->stream; }
 int64_t Runtime::last_launch_count() const { return impl_->launches; }
 size_t Runtime::replica_count() const { return impl_->n; }
+void Runtime::transfer_bytes(int64_t* h2d, int64_t* d2h) const {
+    if (h2d) *h2d = impl_->h2d_bytes;
+    if (d2h) *d2h = impl_->d2h_bytes;
+}
 
 void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n,
                       bool collect) {
@@ -169,6 +277,8 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
         DSD_CUDA(cudaMemcpyAsync(d_gseed, P.gseed.data(), 8 * n, cudaMemcpyHostToDevice, R.stream));
         DSD_CUDA(cudaMemcpyAsync(d_rs, P.rep_scen.data(), 4 * n, cudaMemcpyHostToDevice, R.stream));
     }
+    R.h2d_bytes = static_cast<int64_t>(P.blob.size() + sizeof(DevScenario) * ns + 20 * n);
+    R.d2h_bytes = 0;
     R.summary.ensure(sizeof(DevSummary) * std::max<size_t>(n, 1));
     R.fail.ensure(sizeof(int32_t) * std::max<size_t>(n, 1));
 
@@ -211,7 +321,8 @@ void Runtime::launch() {
     }
     const unsigned grid = static_cast<unsigned>((R.n + kBlock - 1) / kBlock);
     DSD_CUDA(cudaEventRecord(R.ev[0], R.stream));
-    k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, R.collect ? static_cast<int64_t*>(R.ltot.p) : nullptr);
+    k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, R.collect ? static_cast<int64_t*>(R.ltot.p) : nullptr, nullptr,
+                                           nullptr);
     DSD_CUDA(cudaGetLastError());
     ++R.launches;
     if (R.collect) {
@@ -234,10 +345,36 @@ void Runtime::launch() {
         R.W.seq_gamma = static_cast<int32_t*>(R.seqg.p);
         R.W.seq_commit = static_cast<int32_t*>(R.seqc.p);
     }
+    if (R.step_stats) {
+        R.stats.ensure(64 * sizeof(unsigned long long));
+        DSD_CUDA(cudaMemsetAsync(R.stats.p, 0, 64 * sizeof(unsigned long long), R.stream));
+        R.W.step_stats = static_cast<unsigned long long*>(R.stats.p);
+    }
     DSD_CUDA(cudaEventRecord(R.ev[1], R.stream));
-    k_simulate<<<grid, kBlock, 0, R.stream>>>(R.W);
-    DSD_CUDA(cudaGetLastError());
-    ++R.launches;
+    const bool smem = R.W.c.ns <= kSmemServers && R.smem_heap > 0;
+    if (smem) {
+        const size_t bytes = static_cast<size_t>(kBlock / kLanes) *
+                             (static_cast<size_t>(kServerFields) * R.W.c.ns * kLanes * 4 +
+                              static_cast<size_t>(R.smem_heap) * kLanes * 16);
+        k_simulate<true><<<grid, kBlock, bytes, R.stream>>>(R.W, nullptr, nullptr, R.smem_heap);
+        DSD_CUDA(cudaGetLastError());
+        // replicas whose event heap outgrew shared memory run again from HBM
+        R.ovf.ensure(4 * (R.n + 1));
+        int32_t* count = static_cast<int32_t*>(R.ovf.p);
+        int32_t* list = count + 1;
+        DSD_CUDA(cudaMemsetAsync(count, 0, 4, R.stream));
+        const unsigned g2 = static_cast<unsigned>((R.n + 255) / 256);
+        k_collect_overflow<<<g2, 256, 0, R.stream>>>(R.W, list, count);
+        k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, R.collect ? static_cast<int64_t*>(R.ltot.p) : nullptr, list,
+                                                count);
+        k_simulate<false><<<grid, kBlock, 0, R.stream>>>(R.W, list, count, 0);
+        DSD_CUDA(cudaGetLastError());
+        R.launches += 4;
+    } else {
+        k_simulate<false><<<grid, kBlock, 0, R.stream>>>(R.W, nullptr, nullptr, 0);
+        DSD_CUDA(cudaGetLastError());
+        ++R.launches;
+    }
     DSD_CUDA(cudaEventRecord(R.ev[2], R.stream));
     R.ran = true;
 }
@@ -246,6 +383,20 @@ void Runtime::sync() {
     RuntimeImpl& R = *impl_;
     DSD_CUDA(cudaSetDevice(R.device));
     DSD_CUDA(cudaStreamSynchronize(R.stream));
+    if (R.step_stats && R.W.step_stats) {
+        unsigned long long s[64];
+        DSD_CUDA(cudaMemcpy(s, R.stats.p, sizeof(s), cudaMemcpyDeviceToHost));
+        static const char* names[] = {"pop", "arrival", "net_prompt", "net_proposal", "net_result", "begin",
+                                      "compute_done", "item", "finish", "activate", "dispatch", "send_prompt"};
+        unsigned long long steps = 0;
+        for (int k = 0; k < kActKinds; ++k) steps += s[2 * k + 1];
+        std::fprintf(stderr, "[dsd step stats] warp iterations %llu (max %llu), warp cycles %llu, lane steps %llu\n",
+                     s[32], s[34], s[33], steps);
+        for (int k = 0; k < kActKinds; ++k)
+            if (s[2 * k + 1])
+                std::fprintf(stderr, "  %-13s steps %12llu  avg cycles/step %8.1f\n", names[k], s[2 * k + 1],
+                             static_cast<double>(s[2 * k]) / static_cast<double>(s[2 * k + 1]));
+    }
 }
 
 void Runtime::last_kernel_ms(double* sim_ms, double* gen_ms, double* total_ms) {
@@ -267,6 +418,7 @@ void Runtime::summaries(dsd_replica_summary* out, size_t n) {
     if (n > R.n) throw Error(DSD_ERR_RUNTIME, "summary buffer larger than the batch");
     DSD_CUDA(cudaSetDevice(R.device));
     if (n) DSD_CUDA(cudaMemcpyAsync(out, R.summary.p, sizeof(DevSummary) * n, cudaMemcpyDeviceToHost, R.stream));
+    R.d2h_bytes += static_cast<int64_t>(sizeof(DevSummary) * n);
     DSD_CUDA(cudaStreamSynchronize(R.stream));
 }
 

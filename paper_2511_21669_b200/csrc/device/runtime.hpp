@@ -43,6 +43,7 @@ public:
     int64_t last_launch_count() const;
     void last_kernel_ms(double* sim_ms, double* gen_ms, double* total_ms);
     size_t replica_count() const;
+    void transfer_bytes(int64_t* h2d, int64_t* d2h) const;
 
 private:
     std::unique_ptr<RuntimeImpl> impl_;

@@ -140,6 +140,12 @@ int dsd_last_kernel_ms(dsd_handle* h, double* sim_kernel_ms, double* gen_kernel_
     });
 }
 
+int dsd_last_transfer_bytes(dsd_handle* h, int64_t* h2d_bytes, int64_t* d2h_bytes) {
+    if (!h || !h->rt) return DSD_ERR_RUNTIME;
+    h->rt->transfer_bytes(h2d_bytes, d2h_bytes);
+    return DSD_OK;
+}
+
 int dsd_run_simulation(dsd_handle* h, const char* config_yaml, const char* base_dir, int strict, int has_seed,
                        uint64_t seed, char** report_json, char** report_csv, uint64_t* events_processed,
                        int64_t* end_time_us, double* agg, char* err, size_t errlen) {

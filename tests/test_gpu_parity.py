@@ -98,3 +98,21 @@ def test_sweep_report_files_match_reference(sim, tmp_path):
     assert ref_files == sorted(os.listdir(my_dir))
     for f in ref_files:
         assert (ref_dir / f).read_bytes() == (my_dir / f).read_bytes(), f
+
+
+@pytest.mark.parametrize("smem_heap", ["0", "2", "8"])
+def test_kernel_variants_and_overflow_rerun(smem_heap):
+    """HBM variant (0), shared-memory variant with forced heap overflow and
+    HBM re-run (2), default shared-memory variant (8): identical results."""
+    from paper_2511_21669_b200 import Simulator
+    spec = ("base: c1_single_pair.yaml\nseed: 11\nrepetitions: 4\naxes:\n"
+            "  network.jitter_ms: [0, 3]\n  policies.window.gamma: [1, 4, 9]\n"
+            "  workload.rate_rps: [2, 30]\n")
+    js, _ = ref.run_sweep(spec, CFG, 4)
+    os.environ["DSD_SMEM_HEAP"] = smem_heap
+    try:
+        with Simulator(0) as s:
+            out = s.run_sweep(spec, base_dir=CFG)
+    finally:
+        del os.environ["DSD_SMEM_HEAP"]
+    assert out.summary_json == js
