@@ -25,9 +25,19 @@ import time
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 SPEC = os.path.join(REPO, "configs", "c5_sweep_65536.yaml")
+SPEC_DIR = os.path.dirname(SPEC)
+
+
+def sweep_text(world):
+    """The C5 sweep with 16*world repetitions: every rank simulates its own
+    65,536-replica shard (repetitions r, r+world, ...) of one sweep (weak scaling)."""
+    text = open(SPEC).read()
+    assert "repetitions: 16" in text
+    return text.replace("repetitions: 16", f"repetitions: {16 * world}")
 B_EV = 64  # algorithmic replica-state bytes per simulated event (SURVEY §8(d))
 METRIC = "simulated_events_per_sec"
-WORKLOAD = "c5_sweep_65536: 4096 points (gamma 1..16 x rtt 2..32 ms x alpha 0.50..0.95) x 16 reps, C1 single pair"
+WORKLOAD = ("c5_sweep_65536: 4096 points (gamma 1..16 x rtt 2..32 ms x alpha 0.50..0.95) x 16 reps per GPU "
+            "(16*N repetitions sharded by repetition over N GPUs), C1 single edge-cloud pair")
 
 
 def env_int(k, d):
@@ -127,7 +137,7 @@ def cpu_reference(seconds_target=8.0, threads=None):
         L = _lib.lib()
         p = ctypes.c_void_p()
         err = ctypes.create_string_buffer(1024)
-        assert L.dsd_plan_sweep(spec.encode(), base.encode(), ctypes.byref(p), err, 1024) == 0
+        assert L.dsd_plan_sweep(spec.encode(), base.encode(), 0, 1, ctypes.byref(p), err, 1024) == 0
         sc, rp = ctypes.c_void_p(), ctypes.c_void_p()
         L.dsd_sweep_plan_scenarios(p, ctypes.byref(sc))
         nrep = L.dsd_sweep_plan_replicas(p, ctypes.byref(rp))
@@ -167,7 +177,7 @@ def main_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * sec / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64+f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
         "data": "synthetic (reference generate_synthetic streams)",
         "config": {"workload": WORKLOAD, "replicas_sampled_per_step": last["replicas"] if last else 0},
         "replicas_per_sec": rep / sec,
@@ -192,14 +202,15 @@ def main_ours(args, rank, world, local_rank):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     sim = Simulator(local_rank)
-    n_rep, n_pts = sim.prepare_sweep(SPEC, shard=rank, n_shards=world)
+    spec = sweep_text(world)
+    n_rep, n_pts = sim.prepare_sweep(spec, base_dir=SPEC_DIR, shard=rank, n_shards=world)
     stream = torch.cuda.ExternalStream(sim.stream(), device=torch.device("cuda", local_rank))
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     sum_ptr, sum_bytes = sim.device_summaries()
     gather = None
     if world > 1:
         # per-replica summaries, gathered once per step over NVLink
-        max_rep = -(-65536 // world)
+        max_rep = n_rep
         rows = torch.zeros(max_rep * 96, dtype=torch.uint8, device="cuda")
         gather = torch.zeros(world * max_rep * 96, dtype=torch.uint8, device="cuda")
 
@@ -264,10 +275,10 @@ def main_ours(args, rank, world, local_rank):
             dist.barrier()
         t = time.perf_counter()
         if world == 1:
-            out = sim.run_sweep(SPEC)
+            out = sim.run_sweep(spec, base_dir=SPEC_DIR)
             assert out.failed_points == 0
         else:
-            sim.prepare_sweep(SPEC, shard=rank, n_shards=world)
+            sim.prepare_sweep(spec, base_dir=SPEC_DIR, shard=rank, n_shards=world)
             sim.launch()
             s2 = sim.summaries()
             _ = s2["throughput_rps"].sum()
@@ -282,7 +293,7 @@ def main_ours(args, rank, world, local_rank):
         e2e_s = float(t.item())
     # restore the prepared device batch
     if world == 1:
-        sim.prepare_sweep(SPEC, shard=rank, n_shards=world)
+        sim.prepare_sweep(spec, base_dir=SPEC_DIR, shard=rank, n_shards=world)
 
     if rank != 0:
         if dist:
@@ -294,12 +305,13 @@ def main_ours(args, rank, world, local_rank):
     traffic = ncu_traffic()
     line = {
         "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64+f64",
         "data": "synthetic (reference generate_synthetic streams, regenerated on device every step)",
         "config": {"workload": WORKLOAD, "replicas": int(rep_all), "points": n_pts,
                    "events_per_step": int(ev_all), "l2": "flushed between steps (512 MiB memset)",
-                   "parallelism": f"replica shards x{world}"},
+                   "parallelism": f"replica shards x{world} + NCCL all-gather of summaries" if world > 1
+                   else "single GPU"},
         "replicas_per_sec": rep_all / (ms_per_step / 1e3),
         "e2e": {"value": ev_all / e2e_s, "unit": "events/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_s,

@@ -291,11 +291,16 @@ void dsd_resolved_replica(const dsd_resolved* r, dsd_replica* out);
 const char* dsd_resolved_digest(const dsd_resolved* r);
 void dsd_resolved_free(dsd_resolved* r);
 
-/* Resolves a sweep spec (all points and repetitions, point-major order) into
- * scenarios + replicas without running it; the object owns the arrays. */
+/* Resolves a sweep spec into scenarios + replicas without running it (the
+ * object owns the arrays).  Replicas are point-major, repetition-minor; with
+ * n_shards > 1 only replicas g with g % n_shards == shard are kept, exactly
+ * the set dsd_prepare_sweep(shard, n_shards) runs.  dsd_sweep_plan_origin
+ * returns, per kept replica, its (point index, repetition). */
 typedef struct dsd_sweep_plan dsd_sweep_plan;
-int dsd_plan_sweep(const char* sweep_yaml, const char* base_dir, dsd_sweep_plan** out, char* err,
-                   size_t errlen);
+int dsd_plan_sweep(const char* sweep_yaml, const char* base_dir, int shard, int n_shards,
+                   dsd_sweep_plan** out, char* err, size_t errlen);
+size_t dsd_sweep_plan_origin(const dsd_sweep_plan* p, int64_t* point, int32_t* repetition,
+                             size_t cap);
 size_t dsd_sweep_plan_scenarios(const dsd_sweep_plan* p, const dsd_scenario** scenarios);
 size_t dsd_sweep_plan_replicas(const dsd_sweep_plan* p, const dsd_replica** replicas);
 void dsd_sweep_plan_free(dsd_sweep_plan* p);

@@ -58,7 +58,7 @@ EXPORTS = [
     "dsd_last_transfer_bytes",
     "dsd_run_simulation", "dsd_run_sweep", "dsd_prepare_sweep", "dsd_resolve_config", "dsd_resolved_scenario",
     "dsd_resolved_replica", "dsd_resolved_digest", "dsd_resolved_free", "dsd_plan_sweep",
-    "dsd_sweep_plan_scenarios", "dsd_sweep_plan_replicas", "dsd_sweep_plan_free", "dsd_emit_report",
+    "dsd_sweep_plan_scenarios", "dsd_sweep_plan_replicas", "dsd_sweep_plan_origin", "dsd_sweep_plan_free", "dsd_emit_report",
     "dsd_sweep_point_seed", "dsd_free",
 ]
 
@@ -112,7 +112,9 @@ def lib():
     L.dsd_resolved_digest.restype = cp
     L.dsd_resolved_free.argtypes = [vp]
     L.dsd_resolved_free.restype = None
-    L.dsd_plan_sweep.argtypes = [cp, cp, c.POINTER(vp), cp, sz]
+    L.dsd_plan_sweep.argtypes = [cp, cp, c.c_int, c.c_int, c.POINTER(vp), cp, sz]
+    L.dsd_sweep_plan_origin.argtypes = [vp, c.POINTER(c.c_int64), c.POINTER(c.c_int32), sz]
+    L.dsd_sweep_plan_origin.restype = sz
     L.dsd_sweep_plan_scenarios.argtypes = [vp, c.POINTER(vp)]
     L.dsd_sweep_plan_scenarios.restype = sz
     L.dsd_sweep_plan_replicas.argtypes = [vp, c.POINTER(vp)]

@@ -270,6 +270,21 @@ struct Engine {
         st1 = st0;
         st0 = a;
         ++sp;
+        // the action runs a few warp iterations later: start pulling its
+        // request record into L1 now
+        const uint32_t k = a & 15u, arg = a >> 4;
+        if ((k >= kActArrival && k <= kActNetResult) || k == kActFinish || k == kActSendPrompt) {
+            prefetch_record(arg);
+        } else if (k == kActBegin || k == kActItem) {
+            prefetch_record(arg >> 1);
+        }
+    }
+    DSD_HD void prefetch_record(uint32_t i) const {
+#ifdef __CUDA_ARCH__
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(R + i));
+#else
+        (void)i;
+#endif
     }
     DSD_HD uint32_t pop_act() {
         uint32_t a = st0;

@@ -256,11 +256,13 @@ struct dsd_sweep_plan {
     dsd::host::SweepBatch b;
 };
 
-int dsd_plan_sweep(const char* sweep_yaml, const char* base_dir, dsd_sweep_plan** out, char* err, size_t errlen) {
+int dsd_plan_sweep(const char* sweep_yaml, const char* base_dir, int shard, int n_shards, dsd_sweep_plan** out,
+                   char* err, size_t errlen) {
     return guard(err, errlen, [&] {
+        if (n_shards < 1 || shard < 0 || shard >= n_shards) throw dsd::Error(DSD_ERR_CONFIG, "bad shard index");
         dsd::cfg::Node node = dsd::cfg::parse(sweep_yaml ? sweep_yaml : "");
         auto p = std::make_unique<dsd_sweep_plan>();
-        p->b = dsd::host::plan_sweep(node, base_dir ? base_dir : ".", 0, 1, nullptr);
+        p->b = dsd::host::plan_sweep(node, base_dir ? base_dir : ".", shard, n_shards, nullptr);
         for (size_t k = 0; k < p->b.resolved.size(); ++k) {
             p->b.resolved[k].bind();
             p->b.scenarios[k] = p->b.resolved[k].scen;
@@ -277,6 +279,15 @@ size_t dsd_sweep_plan_scenarios(const dsd_sweep_plan* p, const dsd_scenario** sc
 size_t dsd_sweep_plan_replicas(const dsd_sweep_plan* p, const dsd_replica** replicas) {
     if (replicas) *replicas = p->b.replicas.data();
     return p->b.replicas.size();
+}
+
+size_t dsd_sweep_plan_origin(const dsd_sweep_plan* p, int64_t* point, int32_t* repetition, size_t cap) {
+    const auto& o = p->b.replica_origin;
+    for (size_t k = 0; k < o.size() && k < cap; ++k) {
+        if (point) point[k] = o[k].first;
+        if (repetition) repetition[k] = o[k].second;
+    }
+    return o.size();
 }
 
 void dsd_sweep_plan_free(dsd_sweep_plan* p) { delete p; }

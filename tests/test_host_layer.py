@@ -78,7 +78,7 @@ def test_sweep_plan_seeds_match_reference():
     L = _lib.lib()
     p = ctypes.c_void_p()
     err = ctypes.create_string_buffer(1024)
-    assert L.dsd_plan_sweep(spec.encode(), CFG.encode(), ctypes.byref(p), err, 1024) == 0
+    assert L.dsd_plan_sweep(spec.encode(), CFG.encode(), 0, 1, ctypes.byref(p), err, 1024) == 0
     reps = ctypes.c_void_p()
     n = L.dsd_sweep_plan_replicas(p, ctypes.byref(reps))
     assert n == 65536
