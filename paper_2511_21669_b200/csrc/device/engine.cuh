@@ -187,74 +187,83 @@ enum : uint32_t {
 // Actions are kind | arg << 4 (args < 2^28: requests < 2^26, slots < 2^27).
 
 struct Engine {
+    // Register budget: everything below stays live across the whole event
+    // loop, so only what nearly every step touches lives here; counters the
+    // reference keeps incrementally (events processed, first arrival, last
+    // completion, completed) are derived once in finish(), and the routing
+    // stream / round-robin counter (random and rr routing only) live in HBM.
     const Workspace& W;
     const DevScenario& S;
-    const char* blob;
-    Lane L;
-    int64_t rep;
     ReqRec* R;  // this replica's request records
-
-    // replica scalars (registers)
-    int64_t N;
+    int32_t rep;
+    int32_t N;
     int64_t now = 0;
     uint32_t seq_next;  // next seq for schedule(); arrivals hold 0..N-1
-    int64_t heap_n = 0;
-    int64_t next_arr = 0;
-    uint64_t processed = 0;
-    Rng routing, jitter;
-    uint64_t rr_counter = 0;
-    int64_t first_arrival = -1, last_completion = -1;
-    int64_t net_wait_total = 0, net_wait_count = 0;
-    int64_t completed = 0;
+    int32_t heap_n = 0;
+    int32_t next_arr = 0;
+    Rng jitter;
+    int64_t net_wait_total = 0;
+    int32_t net_wait_count = 0;
     int32_t fail = kFailNone;
-    int64_t seqbase = 0;
     int32_t T, D;
     // action stack
     uint32_t st0 = 0, st1 = 0, st2 = 0, st3 = 0;
-    int sp = 0;
+    int32_t sp = 0;
     int32_t item_server = -1;
     // per-warp state blocks (shared memory for small topologies, else HBM),
     // already offset by this lane: element k of a field is at base[k * 32]
     int32_t* sb;     // server fields [kServerFields][nsc]
     int64_t* htb;    // heap times [hcap]
     uint64_t* hkb;   // heap keys  [hcap]
-    int64_t hcap;
+    int32_t hcap;
     int32_t nsc;
-    // hot scenario parameters held in registers
-    int32_t fe, ps, wkind, gamma_s, max_batch, dmax_batch, batching, routing_kind;
-    int64_t win_us;
-    double sim_frac;
+    // hot scenario parameters: packed policy flags + the static window
+    uint32_t pflags;  // fused_everything | pair_stats<<1 | lab<<2 | jitter_free<<3 | window<<4 | routing<<6
+    int32_t gamma_s, max_batch, dmax_batch;
 
     DSD_HD Engine(const Workspace& w, const DevScenario& s, int64_t replica, int32_t* server_base,
                   int64_t* heap_time_base, uint64_t* heap_key_base, int64_t heap_cap, int32_t server_cap)
-        : W(w), S(s), blob(w.blob), rep(replica), sb(server_base), htb(heap_time_base), hkb(heap_key_base),
-          hcap(heap_cap), nsc(server_cap) {
-        L.w = replica / kLanes;
-        L.lane = static_cast<int>(replica % kLanes);
+        : W(w), S(s), rep(static_cast<int32_t>(replica)), sb(server_base), htb(heap_time_base),
+          hkb(heap_key_base), hcap(static_cast<int32_t>(heap_cap)), nsc(server_cap) {
         T = S.n_targets;
         D = S.n_drafts;
         R = W.req + replica * W.c.nr;
-        fe = S.fused_everything;
-        ps = S.pair_stats;
-        wkind = S.window_kind;
+        pflags = static_cast<uint32_t>(S.fused_everything) | (static_cast<uint32_t>(S.pair_stats) << 1) |
+                 (static_cast<uint32_t>(S.batching == 1) << 2) | (static_cast<uint32_t>(S.jitter_free) << 3) |
+                 (static_cast<uint32_t>(S.window_kind) << 4) | (static_cast<uint32_t>(S.routing) << 6);
         gamma_s = S.gamma;
         max_batch = S.max_batch;
         dmax_batch = S.draft_max_batch;
-        batching = S.batching;
-        routing_kind = S.routing;
-        win_us = S.batching_window_us;
-        sim_frac = S.sim_frac;
+    }
+    DSD_HD bool fe() const { return pflags & 1u; }
+    DSD_HD bool ps() const { return (pflags >> 1) & 1u; }
+    DSD_HD bool lab_batching() const { return (pflags >> 2) & 1u; }
+    DSD_HD bool jitter_free() const { return (pflags >> 3) & 1u; }
+    DSD_HD uint32_t wkind() const { return (pflags >> 4) & 3u; }
+    DSD_HD uint32_t routing_kind() const { return (pflags >> 6) & 3u; }
+    // warp-interleaved per-replica arrays in HBM (pair stats, busy export)
+    template <typename U>
+    DSD_HD U& IL(U* base, int64_t cap, int64_t idx) const {
+        return base[((static_cast<int64_t>(rep) >> 5) * cap + idx) * kLanes + (rep & 31)];
     }
 
     // server fields (engine.cpp:70-84 Server, minus the queue/running vectors
     // which are intrusive lists through the request records)
     enum : int {
         F_v_qhead = 0, F_v_qtail, F_v_run, F_v_busy, F_v_armed, F_v_armseq, F_v_active, F_v_shead, F_v_stail,
-        F_v_open
+        F_v_open, F_v_busy_lo, F_v_busy_hi
     };
 #define SV(field, i) sv(F_##field, (i))
     DSD_HD int32_t& sv(int f, int32_t v) const { return sb[(static_cast<int64_t>(f) * nsc + v) * kLanes]; }
-    DSD_HD int64_t& busy_us(int32_t v) const { return L.at(W.v_busy_us, W.c.ns, v); }
+    // Server::busy_us (engine.cpp:562) as two 32-bit halves in the server block
+    DSD_HD int64_t get_busy(int32_t v) const {
+        return static_cast<int64_t>((static_cast<uint64_t>(static_cast<uint32_t>(SV(v_busy_hi, v))) << 32) |
+                                    static_cast<uint32_t>(SV(v_busy_lo, v)));
+    }
+    DSD_HD void set_busy(int32_t v, int64_t x) {
+        SV(v_busy_lo, v) = static_cast<int32_t>(static_cast<uint32_t>(x));
+        SV(v_busy_hi, v) = static_cast<int32_t>(static_cast<uint32_t>(static_cast<uint64_t>(x) >> 32));
+    }
     DSD_HD int64_t& ht(int64_t k) const { return htb[k * kLanes]; }
     DSD_HD uint64_t& hk(int64_t k) const { return hkb[k * kLanes]; }
 
@@ -361,14 +370,17 @@ struct Engine {
     static DSD_HD uint32_t info(uint32_t kind, uint32_t msg, uint32_t id) { return kind | (msg << 3) | (id << 5); }
 
     // ---- network: net_delay (engine.cpp:10-15) ----
-    DSD_HD const double* link(int32_t d, int32_t t) const {
-        const int32_t* dg = blob_ptr<int32_t>(blob, S.o_dgroup);
-        const int32_t* tg = blob_ptr<int32_t>(blob, S.o_tgroup);
-        return blob_ptr<double>(blob, S.o_links) + 2 * (dg[d] * S.n_tg + tg[t]);
+    DSD_HD const DevLink& link(int32_t d, int32_t t) const {
+        const DevLink* links = blob_ptr<DevLink>(W.blob, S.o_links);
+        if (S.n_dg == 1 && S.n_tg == 1) return links[0];
+        const int32_t* dg = blob_ptr<int32_t>(W.blob, S.o_dgroup);
+        const int32_t* tg = blob_ptr<int32_t>(W.blob, S.o_tgroup);
+        return links[dg[d] * S.n_tg + tg[t]];
     }
     DSD_HD int64_t net_delay(int32_t d, int32_t t) {
-        const double* lk = link(d, t);
-        double rtt = lk[0], jit = lk[1];
+        const DevLink& lk = link(d, t);
+        if (jitter_free()) return lk.fixed_us;  // the jitter stream is unobservable
+        double rtt = lk.rtt_ms, jit = lk.jitter_ms;
         double j = jitter.uniform(-jit / 2.0, jit / 2.0);
         double ms = rtt / 2.0 + j;
         if (ms < 0.0) ms = 0.0;
@@ -378,11 +390,11 @@ struct Engine {
     // ---- metrics hooks (metrics.cpp:40-128) ----
     DSD_HD int64_t pair_of(int32_t d, int32_t t) const { return static_cast<int64_t>(d) * T + t; }
     DSD_HD double acceptance_recent(int64_t p) const {
-        int32_t cnt = L.at(W.p_acc_cnt, W.c.np, p);
+        int32_t cnt = IL(W.p_acc_cnt, W.c.np, p);
         int64_t ex = 0, ac = 0;
         for (int k = 0; k < cnt; ++k) {
-            ex += L.at(W.p_acc_ex, W.c.np * 20, p * 20 + k);
-            ac += L.at(W.p_acc_ac, W.c.np * 20, p * 20 + k);
+            ex += IL(W.p_acc_ex, W.c.np * 20, p * 20 + k);
+            ac += IL(W.p_acc_ac, W.c.np * 20, p * 20 + k);
         }
         if (ex == 0) return 0.5;
         return static_cast<double>(ac) / static_cast<double>(ex);
@@ -395,22 +407,22 @@ struct Engine {
         return s;
     }
     DSD_HD void on_verify(int32_t d, int32_t t, int ex, int ac) {
-        if (!ps) return;
+        if (!ps()) return;
         int64_t p = pair_of(d, t);
-        int64_t slot = ring_slot(L.at(W.p_acc_cnt, W.c.np, p), L.at(W.p_acc_pos, W.c.np, p), 20);
-        L.at(W.p_acc_ex, W.c.np * 20, p * 20 + slot) = ex;
-        L.at(W.p_acc_ac, W.c.np * 20, p * 20 + slot) = ac;
+        int64_t slot = ring_slot(IL(W.p_acc_cnt, W.c.np, p), IL(W.p_acc_pos, W.c.np, p), 20);
+        IL(W.p_acc_ex, W.c.np * 20, p * 20 + slot) = ex;
+        IL(W.p_acc_ac, W.c.np * 20, p * 20 + slot) = ac;
     }
     DSD_HD void on_rtt_sample(int32_t d, int32_t t, double rtt_ms) {
-        if (!ps) return;
+        if (!ps()) return;
         int64_t p = pair_of(d, t);
-        int64_t slot = ring_slot(L.at(W.p_rtt_cnt, W.c.np, p), L.at(W.p_rtt_pos, W.c.np, p), 20);
-        L.at(W.p_rtt, W.c.np * 20, p * 20 + slot) = rtt_ms;
+        int64_t slot = ring_slot(IL(W.p_rtt_cnt, W.c.np, p), IL(W.p_rtt_pos, W.c.np, p), 20);
+        IL(W.p_rtt, W.c.np * 20, p * 20 + slot) = rtt_ms;
     }
     DSD_HD void push_tpot(int32_t t, double v) {
-        if (!ps) return;
-        int64_t slot = ring_slot(L.at(W.t_tcnt, W.c.nt, t), L.at(W.t_tpos, W.c.nt, t), 50);
-        L.at(W.t_tpot, W.c.nt * 50, static_cast<int64_t>(t) * 50 + slot) = v;
+        if (!ps()) return;
+        int64_t slot = ring_slot(IL(W.t_tcnt, W.c.nt, t), IL(W.t_tpos, W.c.nt, t), 50);
+        IL(W.t_tpot, W.c.nt * 50, static_cast<int64_t>(t) * 50 + slot) = v;
     }
 
     // ---- window policies: decide_window (engine.cpp:350-374) ----
@@ -422,13 +434,13 @@ struct Engine {
         int32_t d = draft_of(i);
         if (d < 0) return Decision{true, 1};
         int32_t t = R[i].target;
-        switch (wkind) {
+        switch (wkind()) {
             case 0:  // window_static (policies.cpp:55-58)
                 return Decision{false, gamma_s};
             case 1: {  // window_dynamic (policies.cpp:60-68)
                 int64_t p = pair_of(d, t);
                 double a = acceptance_recent(p);
-                int32_t& g = L.at(W.p_dyn, W.c.np, p);
+                int32_t& g = IL(W.p_dyn, W.c.np, p);
                 if (a > 0.75 && g < S.gamma_max) {
                     ++g;
                 } else if (a < 0.25 && g > S.gamma_min) {
@@ -443,32 +455,32 @@ struct Engine {
                 double q = static_cast<double>(SV(v_open, t)) / static_cast<double>(S.queue_capacity);
                 f[0] = q < 0.0 ? 0.0 : (q > 1.0 ? 1.0 : q);
                 f[1] = acceptance_recent(p);
-                int32_t rc = L.at(W.p_rtt_cnt, W.c.np, p);
+                int32_t rc = IL(W.p_rtt_cnt, W.c.np, p);
                 if (rc == 0) {
-                    f[2] = link(d, t)[0];
+                    f[2] = link(d, t).rtt_ms;
                 } else {
                     double sum = 0.0;
-                    for (int k = 0; k < rc; ++k) sum += L.at(W.p_rtt, W.c.np * 20, p * 20 + k);
+                    for (int k = 0; k < rc; ++k) sum += IL(W.p_rtt, W.c.np * 20, p * 20 + k);
                     f[2] = sum / static_cast<double>(rc);
                 }
-                int32_t tc = L.at(W.t_tcnt, W.c.nt, t);
+                int32_t tc = IL(W.t_tcnt, W.c.nt, t);
                 if (tc == 0) {
                     f[3] = 0.0;
                 } else {
                     double sum = 0.0;
-                    for (int k = 0; k < tc; ++k) sum += L.at(W.t_tpot, W.c.nt * 50, static_cast<int64_t>(t) * 50 + k);
+                    for (int k = 0; k < tc; ++k) sum += IL(W.t_tpot, W.c.nt * 50, static_cast<int64_t>(t) * 50 + k);
                     f[3] = sum / static_cast<double>(tc);
                 }
-                f[4] = static_cast<double>(L.at(W.p_gprev, W.c.np, p));
-                double raw = awc_predict(blob, S, f);
+                f[4] = static_cast<double>(IL(W.p_gprev, W.c.np, p));
+                double raw = awc_predict(W.blob, S, f);
                 // stabilized_decide (smoother.cpp:8-37)
                 const double gmin = static_cast<double>(S.gamma_min);
                 const double gmax = static_cast<double>(S.gamma_max);
                 double clamped = raw < gmin ? gmin : (gmax < raw ? gmax : raw);
-                uint8_t& init = L.at(W.p_sm_init, W.c.np, p);
-                double& ema = L.at(W.p_sm_ema, W.c.np, p);
-                int32_t& low = L.at(W.p_sm_low, W.c.np, p);
-                uint8_t& fz = L.at(W.p_sm_fused, W.c.np, p);
+                uint8_t& init = IL(W.p_sm_init, W.c.np, p);
+                double& ema = IL(W.p_sm_ema, W.c.np, p);
+                int32_t& low = IL(W.p_sm_low, W.c.np, p);
+                uint8_t& fz = IL(W.p_sm_fused, W.c.np, p);
                 const double ema_alpha = 0.4;
                 if (!init) {
                     ema = clamped;
@@ -529,28 +541,33 @@ struct Engine {
     DSD_HD void try_dispatch(int32_t v, bool window_expired) {
         if (SV(v_busy, v) || SV(v_qhead, v) < 0) return;
         const bool is_draft = v >= T;
-        int32_t kind = -1;
-        int64_t ncand = 0;
-        for (int32_t cur = SV(v_qhead, v); cur >= 0; cur = slot_next(cur)) {
-            uint32_t op = R[cur >> 1].op[cur & 1] & 3u;
-            if (!eligible(is_draft, op, cur >> 1)) continue;
-            if (kind < 0) kind = static_cast<int32_t>(op);
-            if (static_cast<int32_t>(op) != kind) continue;
-            ++ncand;
-        }
-        if (ncand == 0) return;
         const int64_t mb = is_draft ? dmax_batch : max_batch;
-        if (!is_draft && win_us > 0 && !window_expired && ncand < mb) {
-            if (!SV(v_armed, v)) {
-                SV(v_armed, v) = 1;
-                SV(v_armseq, v) = seq_next;  // stands in for ++window_gen (engine.cpp:512-517)
-                schedule(now + win_us, info(kEvBatchReady, 0, static_cast<uint32_t>(v)));
+        int32_t kind = -1;
+        // Only an armable batching window needs the candidate count before
+        // anything is taken; otherwise the head kind is fixed by the first
+        // eligible item of the single forming pass below.
+        if (!is_draft && S.batching_window_us > 0 && !window_expired) {
+            int64_t ncand = 0;
+            for (int32_t cur = SV(v_qhead, v); cur >= 0; cur = slot_next(cur)) {
+                uint32_t op = R[cur >> 1].op[cur & 1] & 3u;
+                if (!eligible(is_draft, op, cur >> 1)) continue;
+                if (kind < 0) kind = static_cast<int32_t>(op);
+                if (static_cast<int32_t>(op) != kind) continue;
+                ++ncand;
             }
-            return;
+            if (ncand == 0) return;
+            if (ncand < mb) {
+                if (!SV(v_armed, v)) {
+                    SV(v_armed, v) = 1;
+                    SV(v_armseq, v) = seq_next;  // stands in for ++window_gen (engine.cpp:512-517)
+                    schedule(now + S.batching_window_us, info(kEvBatchReady, 0, static_cast<uint32_t>(v)));
+                }
+                return;
+            }
+            SV(v_armed, v) = 0;
         }
-        SV(v_armed, v) = 0;
 
-        const bool lab = !is_draft && batching == 1;
+        const bool lab = !is_draft && lab_batching();
         int64_t head_len = 0;
         double band = 0.0;
         int64_t taken = 0, seen = 0;
@@ -565,7 +582,9 @@ struct Engine {
             const uint32_t opv = r.op[k];
             const uint32_t op = opv & 3u;
             bool take = false;
-            if (static_cast<int32_t>(op) == kind && eligible(is_draft, op, i)) {
+            const bool elig = eligible(is_draft, op, i);
+            if (elig && kind < 0) kind = static_cast<int32_t>(op);
+            if (static_cast<int32_t>(op) == kind && elig) {
                 if (!lab) {  // batch_fifo (policies.cpp:30-38)
                     take = taken < mb;
                 } else {     // batch_lab (policies.cpp:40-53)
@@ -573,7 +592,7 @@ struct Engine {
                                                   : static_cast<int64_t>(r.output) - r.tokens;
                     if (seen == 0) {
                         head_len = wl;
-                        band = sim_frac * static_cast<double>(head_len);
+                        band = S.sim_frac * static_cast<double>(head_len);
                         take = true;
                     } else if (taken < mb) {
                         double diff = fabs(static_cast<double>(wl - head_len));
@@ -606,10 +625,11 @@ struct Engine {
             }
             cur = nxt;
         }
+        if (taken == 0) return;  // nothing eligible (the reference's empty candidate list)
         // LatencyProfile::predict (profile.cpp:129-151) on the server's grids
-        const int32_t* gi = is_draft ? blob_ptr<int32_t>(blob, S.o_dgrid) + 2 * (v - T)
-                                     : blob_ptr<int32_t>(blob, S.o_tgrid) + 2 * v;
-        const DevGrid* grids = blob_ptr<DevGrid>(blob, S.o_grids);
+        const int32_t* gi = is_draft ? blob_ptr<int32_t>(W.blob, S.o_dgrid) + 2 * (v - T)
+                                     : blob_ptr<int32_t>(W.blob, S.o_tgrid) + 2 * v;
+        const DevGrid* grids = blob_ptr<DevGrid>(W.blob, S.o_grids);
         const bool prefill = kind == static_cast<int32_t>(kOpPrefill);
         const bool decode = kind == static_cast<int32_t>(kOpDecode);
         // queries: (batch, prompt tokens) / (batch, context) / (batch*tokens, context)
@@ -617,13 +637,13 @@ struct Engine {
         const int64_t qc = prefill ? static_cast<int64_t>(tok) : ctx;
         const DevGrid& g = grids[gi[prefill ? 0 : 1]];
         double ms = g.o_btab >= 0 && g.o_ctab >= 0
-                        ? grid_interpolate_int(blob, g, qb, qc)
-                        : grid_interpolate(blob, g, static_cast<double>(qb), static_cast<double>(qc));
+                        ? grid_interpolate_int(W.blob, g, qb, qc)
+                        : grid_interpolate(W.blob, g, static_cast<double>(qb), static_cast<double>(qc));
         if (decode) ms *= tok;
         int64_t lat = llround(ms * 1000.0);
         if (lat < 1) lat = 1;
         SV(v_busy, v) = 1;
-        busy_us(v) += lat;
+        set_busy(v, get_busy(v) + lat);
         schedule(now + lat, info(kEvComputeDone, 0, static_cast<uint32_t>(v)));
     }
 
@@ -631,7 +651,7 @@ struct Engine {
     DSD_HD void record_gamma(int64_t i, int g) {
         int32_t n = R[i].ng;
         if (W.collect) {
-            int64_t o = seqbase + R[i].seqoff + n;
+            int64_t o = W.rep_seqbase[rep] + R[i].seqoff + n;
             if (o < W.seq_cap) W.seq_gamma[o] = g; else fail = kFailSeq;
         }
         R[i].ng = n + 1;
@@ -639,7 +659,7 @@ struct Engine {
     DSD_HD void record_commit(int64_t i, int c) {
         int32_t n = R[i].nc;
         if (W.collect) {
-            int64_t o = seqbase + R[i].seqoff + n;
+            int64_t o = W.rep_seqbase[rep] + R[i].seqoff + n;
             if (o < W.seq_cap) W.seq_commit[o] = c; else fail = kFailSeq;
         }
         R[i].nc = n + 1;
@@ -659,11 +679,20 @@ struct Engine {
 
     // route (engine.cpp:315-330, policies.cpp:9-28)
     DSD_HD int32_t route() {
-        switch (routing_kind) {
-            case 0:
-                return static_cast<int32_t>(routing.below(static_cast<uint64_t>(T)));
+        if (T <= 1) return 0;  // uniform_below(1) draws nothing; rr and jsq pick 0 too
+        uint64_t* st = W.route_state + static_cast<int64_t>(rep) * 5;  // routing stream + rr counter
+        switch (routing_kind()) {
+            case 0: {
+                Rng g{st[0], st[1], st[2], st[3]};
+                const int32_t t = static_cast<int32_t>(g.below(static_cast<uint64_t>(T)));
+                st[0] = g.s0;
+                st[1] = g.s1;
+                st[2] = g.s2;
+                st[3] = g.s3;
+                return t;
+            }
             case 1:
-                return static_cast<int32_t>(rr_counter++ % static_cast<uint64_t>(T));
+                return static_cast<int32_t>(st[4]++ % static_cast<uint64_t>(T));
             default: {
                 int32_t best = 0;
                 int32_t bd = SV(v_open, 0);
@@ -685,9 +714,8 @@ struct Engine {
         int32_t t = route();
         R[i].target = t;
         ++SV(v_open, t);  // MetricsCollector::on_route
-        if (first_arrival < 0 || now < first_arrival) first_arrival = now;
         set_phase(i, kPhQueuedPrefill);
-        if (fe) {
+        if (fe()) {
             set_flag(i, kFused, true);
             enqueue(t, i, 0, kOpPrefill, R[i].prompt, false);
         } else {
@@ -709,7 +737,7 @@ struct Engine {
         if (phase(i) == kPhDone) return;
         int32_t d = draft_of(i);
         int32_t t = R[i].target;
-        if (d >= 0 && t >= 0 && ps) L.at(W.p_gprev, W.c.np, pair_of(d, t)) = dec.fused ? 1 : dec.gamma;
+        if (d >= 0 && t >= 0 && ps()) IL(W.p_gprev, W.c.np, pair_of(d, t)) = dec.fused ? 1 : dec.gamma;
         if (dec.fused) {
             set_flag(i, kFused, true);
             record_gamma(i, 0);
@@ -731,12 +759,10 @@ struct Engine {
         set_phase(i, kPhDone);
         const int32_t t = r.target;
         --SV(v_open, t);
-        if (r.output >= 2 && ps) {
+        if (r.output >= 2 && ps()) {
             double tpot = (static_cast<double>(now - r.first) / 1000.0) / static_cast<double>(r.output - 1);
             push_tpot(t, tpot);
         }
-        if (now > last_completion) last_completion = now;
-        ++completed;
         int32_t d = draft_of(i);
         if (d >= 0) {
             int32_t v = T + d;
@@ -803,7 +829,7 @@ struct Engine {
             set_flag(i, kTpd, true);
             if (r.output == 0) {
                 if (phase(i) != kPhDone) push_act(act(kActFinish, static_cast<uint32_t>(i)));
-            } else if (flag(i, kFused) && fe) {
+            } else if (flag(i, kFused) && fe()) {
                 push_act(act(kActBegin, static_cast<uint32_t>(i) * 2));
             }
         } else if (op == kOpVerify) {
@@ -821,7 +847,7 @@ struct Engine {
             if (commit_tokens(i, 1)) {
                 push_act(act(kActFinish, static_cast<uint32_t>(i)));
             } else {
-                const bool decide = !(fe || draft_of(i) < 0);
+                const bool decide = !(fe() || draft_of(i) < 0);
                 push_act(act(kActBegin, static_cast<uint32_t>(i) * 2 + (decide ? 1u : 0u)));
             }
         }
@@ -830,11 +856,19 @@ struct Engine {
     // ---- setup + SimKernel::run_until (event_queue.cpp:28-42) ----
     DSD_HD void init() {
         const uint64_t seed = W.rep_seed[rep];
-        routing.seed(seed, kLabelRouting);
+        if (T > 1 && routing_kind() <= 1) {  // the routing stream / rr counter live in HBM
+            Rng g;
+            g.seed(seed, kLabelRouting);
+            uint64_t* st = W.route_state + static_cast<int64_t>(rep) * 5;
+            st[0] = g.s0;
+            st[1] = g.s1;
+            st[2] = g.s2;
+            st[3] = g.s3;
+            st[4] = 0;
+        }
         jitter.seed(seed, kLabelJitter);
         N = (S.workload == 0) ? S.n_requests : S.tr_n;
         seq_next = static_cast<uint32_t>(N);
-        if (W.collect) seqbase = W.rep_seqbase[rep];
         for (int32_t v = 0; v < T + D; ++v) {
             SV(v_qhead, v) = -1;
             SV(v_qtail, v) = -1;
@@ -842,35 +876,35 @@ struct Engine {
             SV(v_busy, v) = 0;
             SV(v_armed, v) = 0;
             SV(v_armseq, v) = 0;
-            busy_us(v) = 0;
+            set_busy(v, 0);
             SV(v_active, v) = -1;
             SV(v_shead, v) = -1;
             SV(v_stail, v) = -1;
             SV(v_open, v) = 0;
         }
-        if (ps) {
+        if (ps()) {
             for (int32_t t = 0; t < T; ++t) {
-                L.at(W.t_tcnt, W.c.nt, t) = 0;
-                L.at(W.t_tpos, W.c.nt, t) = 0;
+                IL(W.t_tcnt, W.c.nt, t) = 0;
+                IL(W.t_tpos, W.c.nt, t) = 0;
             }
             int64_t np = static_cast<int64_t>(T) * D;
             for (int64_t p = 0; p < np; ++p) {
-                L.at(W.p_acc_cnt, W.c.np, p) = 0;
-                L.at(W.p_acc_pos, W.c.np, p) = 0;
-                L.at(W.p_rtt_cnt, W.c.np, p) = 0;
-                L.at(W.p_rtt_pos, W.c.np, p) = 0;
-                L.at(W.p_gprev, W.c.np, p) = S.gamma;
-                L.at(W.p_dyn, W.c.np, p) = S.gamma;
-                L.at(W.p_sm_init, W.c.np, p) = 0;
-                L.at(W.p_sm_ema, W.c.np, p) = 0.0;
-                L.at(W.p_sm_low, W.c.np, p) = 0;
-                L.at(W.p_sm_fused, W.c.np, p) = 0;
+                IL(W.p_acc_cnt, W.c.np, p) = 0;
+                IL(W.p_acc_pos, W.c.np, p) = 0;
+                IL(W.p_rtt_cnt, W.c.np, p) = 0;
+                IL(W.p_rtt_pos, W.c.np, p) = 0;
+                IL(W.p_gprev, W.c.np, p) = S.gamma;
+                IL(W.p_dyn, W.c.np, p) = S.gamma;
+                IL(W.p_sm_init, W.c.np, p) = 0;
+                IL(W.p_sm_ema, W.c.np, p) = 0.0;
+                IL(W.p_sm_low, W.c.np, p) = 0;
+                IL(W.p_sm_fused, W.c.np, p) = 0;
             }
         }
     }
 
     DSD_HD int64_t arrival_index(int64_t k) const {
-        if (S.has_order) return blob_ptr<int64_t>(blob, S.o_tr_order)[k];
+        if (S.has_order) return blob_ptr<int64_t>(W.blob, S.o_tr_order)[k];
         return k;
     }
 
@@ -895,7 +929,6 @@ struct Engine {
         if (have_arr && (heap_n == 0 || ta <= ht(0))) {
             ++next_arr;
             now = ta;
-            ++processed;
             push_act(act(kActArrival, static_cast<uint32_t>(ai)));
             return;
         }
@@ -903,7 +936,6 @@ struct Engine {
         const uint64_t key = hk(0);
         heap_pop();
         now = t;
-        ++processed;
         const uint32_t inf = static_cast<uint32_t>(key);
         const uint32_t kind = inf & 7u;
         const uint32_t msg = (inf >> 3) & 3u;
@@ -957,7 +989,7 @@ struct Engine {
             }
             case kActNetResult: {  // on_result_at_draft (engine.cpp:428-435)
                 ReqRec& r = R[arg];
-                if (ps)
+                if (ps())
                     on_rtt_sample(r.drafter, r.target, static_cast<double>(static_cast<int64_t>(r.outd) + r.backd) / 1000.0);
                 if (commit_tokens(arg, r.lcr)) {
                     push_act(act(kActFinish, arg));
@@ -991,26 +1023,30 @@ struct Engine {
 
     // Engine::finish (engine.cpp:648-669) + aggregate_run (runner.cpp:153-169)
     DSD_HD void finish() {
+        for (int32_t v = 0; v < T; ++v) IL(W.v_busy_us, W.c.ns, v) = get_busy(v);  // for the records export
         DevSummary s;
-        s.events_processed = processed;
+        // every pop is one schedule() or one arrival (event_queue.cpp:38):
+        // arrivals popped + dynamic events scheduled - still pending
+        s.events_processed = static_cast<uint64_t>(next_arr) + (seq_next - static_cast<uint32_t>(N)) -
+                             static_cast<uint64_t>(heap_n);
         s.end_time_us = now;
-        s.completed = completed;
-        s.first_arrival_us = first_arrival;
-        s.last_completion_us = last_completion;
         s.net_queue_wait_total_us = net_wait_total;
         s.net_queue_wait_count = net_wait_count;
         s.n_requests = N;
-        s.has_duration = (completed > 0 && last_completion > first_arrival) ? 1 : 0;
-        s.throughput_rps = 0.0;
-        if (s.has_duration) {
-            int64_t dur = last_completion - first_arrival;
-            s.throughput_rps = static_cast<double>(completed) / (static_cast<double>(dur) / 1e6);
+        // MetricsCollector's first_arrival_ (min over routed arrivals),
+        // last_completion_ and records_.size() (metrics.cpp:47-89)
+        int64_t first_arrival = -1, last_completion = -1, completed = 0;
+        for (int32_t k = 0; k < next_arr; ++k) {
+            const int64_t a = R[k].arrival;
+            if (first_arrival < 0 || a < first_arrival) first_arrival = a;
         }
         double ttft = 0.0, tpot = 0.0;
         int64_t n_tpot = 0, n_rec = 0;
         for (int64_t i = 0; i < N; ++i) {  // records sorted by request id
             const ReqRec& r = R[i];
             if (r.done < 0) continue;
+            ++completed;
+            if (r.done > last_completion) last_completion = r.done;
             ++n_rec;
             ttft += static_cast<double>(r.first - r.arrival) / 1000.0;
             if (r.output >= 2) {
@@ -1020,6 +1056,15 @@ struct Engine {
         }
         s.mean_ttft_ms = n_rec > 0 ? ttft / static_cast<double>(n_rec) : 0.0;
         s.mean_tpot_ms = n_tpot > 0 ? tpot / static_cast<double>(n_tpot) : 0.0;
+        s.completed = completed;
+        s.first_arrival_us = first_arrival;
+        s.last_completion_us = last_completion;
+        s.has_duration = (completed > 0 && last_completion > first_arrival) ? 1 : 0;
+        s.throughput_rps = 0.0;
+        if (s.has_duration) {
+            int64_t dur = last_completion - first_arrival;
+            s.throughput_rps = static_cast<double>(completed) / (static_cast<double>(dur) / 1e6);
+        }
         s.status = fail ? 3 : 0;
         W.summary[rep] = s;
         W.fail[rep] = fail;

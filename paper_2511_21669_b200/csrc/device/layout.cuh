@@ -16,7 +16,7 @@ namespace dsd {
 
 constexpr int kLanes = 32;
 constexpr int kMaxHidden = 64;  // AWC hidden width supported by the engine
-constexpr int kServerFields = 10;
+constexpr int kServerFields = 12;
 // Shared-memory variant of the simulation kernel: per-warp server state and a
 // heap of kSmemHeap slots live in shared memory; a replica whose dynamic event
 // heap outgrows it is re-run on the HBM variant.
@@ -47,6 +47,11 @@ enum : int32_t { kFailNone = 0, kFailHeap = 1, kFailAwcDims = 2, kFailSeq = 3, k
 struct AxisSeg {
     int32_t lo, hi;
     double t;
+};
+
+struct DevLink {  // LinkSpec (topology.hpp:25-30) + the jitter-free delay
+    double rtt_ms, jitter_ms;
+    int64_t fixed_us;
 };
 
 struct DevGrid {
@@ -80,6 +85,7 @@ struct DevScenario {
     int64_t o_awc_params;
     double awc_lo[5], awc_hi[5];
     int32_t awc_log[5], has_order;
+    int32_t jitter_free, pad0;  // every link has jitter 0: net_delay is DevLink::fixed_us
     // trace (TRACE / TRACE_POISSON)
     int64_t tr_n;
     int64_t o_tr_prompt, o_tr_output, o_tr_arrival, o_tr_drafter, o_tr_bitoff, o_tr_bits, o_tr_order;
@@ -156,6 +162,9 @@ struct Workspace {
     // FIFO head/tail, open requests); used when the batch runs the HBM variant
     int32_t* srv;
     int64_t* v_busy_us;
+    // routing stream (4 words) + round-robin counter, replica-contiguous [n][5];
+    // touched only by random / rr routing over more than one target
+    uint64_t* route_state;
     // ---- per target TPOT ring (cap nt*50) and per pair stats (cap np) ----
     double* t_tpot;
     int32_t* t_tpos;     // cap nt

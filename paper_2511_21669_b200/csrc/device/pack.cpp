@@ -118,7 +118,21 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
                 if (!(s.links[l].rtt_ms <= 2.0e6))
                     throw Error(DSD_ERR_RUNTIME, "link rtt_ms above the engine limit of 2e6 ms");
             }
-            d.o_links = B.put(s.links, sizeof(dsd_link) * (s.n_drafts > 0 ? nl : 1));
+            // device links carry the constant one-way delay of jitter-free links:
+            // net_delay = llround((rtt/2 + U(-0, 0)) * 1000) = llround((rtt/2 + 0.0) * 1000)
+            // (engine.cpp:10-15); when every link is jitter-free the jitter stream
+            // is never observable, so the engine skips its draws.
+            const size_t ndev = s.n_drafts > 0 ? nl : 1;
+            std::vector<DevLink> dl(ndev);
+            bool jitter_free = true;
+            for (size_t l = 0; l < ndev; ++l) {
+                dl[l].rtt_ms = s.links[l].rtt_ms;
+                dl[l].jitter_ms = s.links[l].jitter_ms;
+                dl[l].fixed_us = std::llround((s.links[l].rtt_ms / 2.0 + 0.0) * 1000.0);
+                if (s.links[l].jitter_ms != 0.0) jitter_free = false;
+            }
+            d.o_links = B.put(dl.data(), sizeof(DevLink) * ndev, false);
+            d.jitter_free = jitter_free ? 1 : 0;
         }
         // grids
         if (s.n_grids < 1 || !s.grids) cfg_error(where + "latency profile has no grids");
@@ -337,6 +351,7 @@ size_t layout_workspace(Workspace& W, const Caps& c, char* base) {
     field(W.req, c.nr);
     field(W.srv, kServerFields * c.ns);
     field(W.v_busy_us, c.ns);
+    field(W.route_state, 5);  // sized lanes x 5, indexed replica-contiguous
     if (c.np > 0) {
         field(W.t_tpot, c.nt * 50); field(W.t_tpos, c.nt); field(W.t_tcnt, c.nt);
         field(W.p_acc_ex, c.np * 20); field(W.p_acc_ac, c.np * 20); field(W.p_acc_pos, c.np);

@@ -60,12 +60,13 @@ __global__ void __launch_bounds__(kBlock) k_stage(Workspace W, int64_t* ltot, co
 }
 
 // One thread per replica; each iteration the warp runs ONE kind of step, for
-// the lanes whose next step is of that kind.  Kinds are visited in a cyclic
-// sweep (one __reduce_or_sync finds the next kind any lane has pending), in
-// lifecycle order, so a lane typically advances through a whole event per
-// sweep and lanes fall into phase with each other.  Replicas are independent,
-// so reordering steps across lanes is free; the warp executes one handler
-// body per iteration instead of the union of all of them.
+// the lanes whose next step is of that kind: the kind most lanes have pending
+// (__match_any_sync + __reduce_max_sync).  Replicas are independent, so
+// reordering steps across lanes is free, while lanes that wait for the
+// popular kind fall into phase with each other - the warp executes one handler
+// body per iteration instead of the union of all of them.  (Measured on the
+// C5 sweep: majority + chaining to the next pop/dispatch beat a cyclic sweep
+// over kinds and un-chained stepping.)
 //
 // kSmem: the warp's server state and the first `heap_cap` event-heap slots
 // live in shared memory (small topologies, <= kSmemServers servers); a replica
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(kBlock) k_stage(Workspace W, int64_t* ltot, co
 //
 // __launch_bounds__(64, 8): <= 128 registers, so 8 blocks (16 warps) fit per
 // SM and a 65,536-replica sweep (13.8 warps/SM on 148 SMs) is one wave.
-template <bool kSmem>
+template <bool kSmem, bool kStats>
 __global__ void __launch_bounds__(kBlock, 8) k_simulate(Workspace W, const int32_t* list, const int32_t* count,
                                                      int32_t smem_heap_cap) {
     int64_t rep = 0;
@@ -106,34 +107,50 @@ __global__ void __launch_bounds__(kBlock, 8) k_simulate(Workspace W, const int32
     Engine e(W, W.scen[W.rep_scen[r]], r, sbase, hb, kb, hcap, nsc);
     if (live) e.init();
     uint32_t kind = live ? e.next_kind() : static_cast<uint32_t>(kActNone);
-    uint32_t sweep = 0;  // next kind the warp considers
-    unsigned long long* stats = W.step_stats;  // optional per-kind cycle profile
-    long long t_start = stats ? clock64() : 0;
+    // kStats: per-step-kind cycle profile (DSD_STEP_STATS=1), one block-level
+    // accumulation, flushed once per block
+    __shared__ unsigned long long blk_stats[kStats ? 2 * kActKinds : 1];
+    long long t_start = 0;
     unsigned long long iters = 0;
+    if constexpr (kStats) {
+        for (int k = threadIdx.x; k < 2 * kActKinds; k += blockDim.x) blk_stats[k] = 0;
+        __syncthreads();
+        t_start = clock64();
+    }
     for (;;) {
-        const unsigned present = __reduce_or_sync(0xffffffffu, kind == kActNone ? 0u : (1u << kind));
-        if (present == 0u) break;
-        const unsigned twice = present | (present << kActKinds);  // cyclic scan from `sweep`
-        const uint32_t pick = (sweep + __ffs(twice >> sweep) - 1) % kActKinds;
-        if (kind == pick) {
-            if (stats) {
+        // the kind most lanes have pending (majority vote)
+        const unsigned peers = __match_any_sync(0xffffffffu, kind);
+        const unsigned score = kind == kActNone ? 0u : ((static_cast<unsigned>(__popc(peers)) << 4) | kind);
+        const unsigned best = __reduce_max_sync(0xffffffffu, score);
+        if (best == 0u) break;
+        if (kind == (best & 15u)) {
+            if constexpr (kStats) {
                 const long long t0 = clock64();
                 e.step();
                 const long long t1 = clock64();
-                atomicAdd(&stats[2 * pick], static_cast<unsigned long long>(t1 - t0));
-                atomicAdd(&stats[2 * pick + 1], 1ull);
+                atomicAdd(&blk_stats[2 * kind], static_cast<unsigned long long>(t1 - t0));
+                atomicAdd(&blk_stats[2 * kind + 1], 1ull);
+                kind = e.next_kind();
             } else {
-                e.step();
+                // the selected lanes run their continuation chain up to the
+                // next pop or dispatch: two "barrier" kinds per event keep the
+                // warp's lanes in phase, the short handlers in between ride along
+                do {
+                    e.step();
+                    kind = e.next_kind();
+                } while (kind != kActPop && kind != kActDispatch && kind != kActNone);
             }
-            kind = e.next_kind();
         }
-        sweep = pick + 1 == kActKinds ? 0 : pick + 1;
-        ++iters;
+        if constexpr (kStats) ++iters;
     }
-    if (stats && (threadIdx.x % kLanes) == 0) {
-        atomicAdd(&stats[32], iters);                                                    // warp iterations
-        atomicAdd(&stats[33], static_cast<unsigned long long>(clock64() - t_start));  // warp cycles
-        atomicMax(&stats[34], iters);
+    if constexpr (kStats) {
+        if ((threadIdx.x % kLanes) == 0) {
+            atomicAdd(&W.step_stats[32], iters);
+            atomicAdd(&W.step_stats[33], static_cast<unsigned long long>(clock64() - t_start));
+            atomicMax(&W.step_stats[34], iters);
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < 2 * kActKinds; k += blockDim.x) atomicAdd(&W.step_stats[k], blk_stats[k]);
     }
     if (live) e.finish();
 }
@@ -356,7 +373,7 @@ void Runtime::launch() {
         const size_t bytes = static_cast<size_t>(kBlock / kLanes) *
                              (static_cast<size_t>(kServerFields) * R.W.c.ns * kLanes * 4 +
                               static_cast<size_t>(R.smem_heap) * kLanes * 16);
-        k_simulate<true><<<grid, kBlock, bytes, R.stream>>>(R.W, nullptr, nullptr, R.smem_heap);
+        (R.step_stats ? k_simulate<true, true> : k_simulate<true, false>)<<<grid, kBlock, bytes, R.stream>>>(R.W, nullptr, nullptr, R.smem_heap);
         DSD_CUDA(cudaGetLastError());
         // replicas whose event heap outgrew shared memory run again from HBM
         R.ovf.ensure(4 * (R.n + 1));
@@ -367,11 +384,11 @@ void Runtime::launch() {
         k_collect_overflow<<<g2, 256, 0, R.stream>>>(R.W, list, count);
         k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, R.collect ? static_cast<int64_t*>(R.ltot.p) : nullptr, list,
                                                 count);
-        k_simulate<false><<<grid, kBlock, 0, R.stream>>>(R.W, list, count, 0);
+        (R.step_stats ? k_simulate<false, true> : k_simulate<false, false>)<<<grid, kBlock, 0, R.stream>>>(R.W, list, count, 0);
         DSD_CUDA(cudaGetLastError());
         R.launches += 4;
     } else {
-        k_simulate<false><<<grid, kBlock, 0, R.stream>>>(R.W, nullptr, nullptr, 0);
+        (R.step_stats ? k_simulate<false, true> : k_simulate<false, false>)<<<grid, kBlock, 0, R.stream>>>(R.W, nullptr, nullptr, 0);
         DSD_CUDA(cudaGetLastError());
         ++R.launches;
     }
