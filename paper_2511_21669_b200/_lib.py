@@ -8,7 +8,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdsdsim.so")
+# DSD_LIB: load another build of the same library (A/B timing of kernel variants).
+LIB_PATH = os.environ.get("DSD_LIB") or os.path.join(HERE, "libdsdsim.so")
 
 DSD_OK = 0
 DSD_ERR_CONFIG = 2

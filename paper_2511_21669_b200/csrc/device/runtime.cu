@@ -249,6 +249,11 @@ Runtime::Runtime(int device) : impl_(new RuntimeImpl) {
     DSD_CUDA(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking));
     if (const char* h = std::getenv("DSD_SMEM_HEAP")) impl_->smem_heap = std::max(0, std::atoi(h));
     if (const char* s = std::getenv("DSD_STEP_STATS")) impl_->step_stats = std::atoi(s) != 0;
+    if (const char* s = std::getenv("DSD_CARVEOUT")) {  // shared-memory share of the L1/smem array (%)
+        const int pct = std::atoi(s);
+        DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        DSD_CUDA(cudaFuncSetAttribute(k_simulate<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    }
     for (auto& ev : impl_->ev) DSD_CUDA(cudaEventCreate(&ev));
 }
 
