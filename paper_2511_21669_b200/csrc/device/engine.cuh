@@ -195,6 +195,9 @@ struct Engine {
     const Workspace& W;
     const DevScenario& S;
     ReqRec* R;  // this replica's request records
+    // shared-memory copies of the draft servers' active sessions (slot d =
+    // draft d, lane stride kHotStride), or null: see rec()
+    unsigned char* hotb;
     int32_t rep;
     int32_t N;
     int64_t now = 0;
@@ -222,12 +225,14 @@ struct Engine {
     int32_t gamma_s, max_batch, dmax_batch;
 
     DSD_HD Engine(const Workspace& w, const DevScenario& s, int64_t replica, int32_t* server_base,
-                  int64_t* heap_time_base, uint64_t* heap_key_base, int64_t heap_cap, int32_t server_cap)
+                  int64_t* heap_time_base, uint64_t* heap_key_base, int64_t heap_cap, int32_t server_cap,
+                  unsigned char* hot_base = nullptr)
         : W(w), S(s), rep(static_cast<int32_t>(replica)), sb(server_base), htb(heap_time_base),
           hkb(heap_key_base), hcap(static_cast<int32_t>(heap_cap)), nsc(server_cap) {
         T = S.n_targets;
         D = S.n_drafts;
         R = W.req + replica * W.c.nr;
+        hotb = S.fused_everything ? nullptr : hot_base;
         pflags = static_cast<uint32_t>(S.fused_everything) | (static_cast<uint32_t>(S.pair_stats) << 1) |
                  (static_cast<uint32_t>(S.batching == 1) << 2) | (static_cast<uint32_t>(S.jitter_free) << 3) |
                  (static_cast<uint32_t>(S.window_kind) << 4) | (static_cast<uint32_t>(S.routing) << 6);
@@ -290,6 +295,9 @@ struct Engine {
     }
     DSD_HD void prefetch_record(uint32_t i) const {
 #ifdef __CUDA_ARCH__
+        if (hotb)  // an active session lives in shared memory
+            for (int32_t d = 0; d < D; ++d)
+                if (SV(v_active, T + d) == static_cast<int32_t>(i)) return;
         asm volatile("prefetch.global.L1 [%0];" ::"l"(R + i));
 #else
         (void)i;
@@ -306,14 +314,39 @@ struct Engine {
 
     // ---- request flags ----
     static constexpr int kDpd = 3, kTpd = 4, kFused = 5;
-    DSD_HD uint32_t phase(int64_t i) const { return R[i].flags & 7u; }
-    DSD_HD void set_phase(int64_t i, uint32_t p) { R[i].flags = static_cast<uint8_t>((R[i].flags & ~7u) | p); }
-    DSD_HD bool flag(int64_t i, int bit) const { return (R[i].flags >> bit) & 1u; }
-    DSD_HD void set_flag(int64_t i, int bit, bool v) {
-        uint8_t f = R[i].flags;
-        R[i].flags = static_cast<uint8_t>(v ? (f | (1u << bit)) : (f & ~(1u << bit)));
+    static DSD_HD uint32_t phase(const ReqRec& r) { return r.flags & 7u; }
+    static DSD_HD void set_phase(ReqRec& r, uint32_t p) { r.flags = static_cast<uint8_t>((r.flags & ~7u) | p); }
+    static DSD_HD bool flag(const ReqRec& r, int bit) { return (r.flags >> bit) & 1u; }
+    static DSD_HD void set_flag(ReqRec& r, int bit, bool v) {
+        uint8_t f = r.flags;
+        r.flags = static_cast<uint8_t>(v ? (f | (1u << bit)) : (f & ~(1u << bit)));
     }
-    DSD_HD int32_t draft_of(int64_t i) const { return D > 0 ? R[i].drafter : -1; }
+    DSD_HD int32_t draft_of(int64_t i) const { return D > 0 ? rec(i).drafter : -1; }
+
+    // ---- request records ----
+    // On sm_100 a global store invalidates its line in L1, so a record that
+    // is read-modify-written every step would cost an L2 round trip per step.
+    // A draft server's active session (the request in its speculation loop,
+    // which takes nearly all record traffic) is therefore moved into a
+    // shared-memory slot while it is active: activate_next_session copies it
+    // in, finish_request writes it back.  rec(i) is the only way the engine
+    // touches a record; the slot is authoritative while i is active.
+    DSD_HD ReqRec& slot(int32_t d) const {
+        return *reinterpret_cast<ReqRec*>(hotb + static_cast<int64_t>(d) * kLanes * kHotStride);
+    }
+    DSD_HD ReqRec& rec(int64_t i) const {
+        if (hotb) {
+            for (int32_t d = 0; d < D; ++d)
+                if (SV(v_active, T + d) == static_cast<int32_t>(i)) return slot(d);
+        }
+        return R[i];
+    }
+    static DSD_HD void copy_rec(ReqRec& dst, const ReqRec& src) {
+        uint64_t* d = reinterpret_cast<uint64_t*>(&dst);
+        const uint64_t* s = reinterpret_cast<const uint64_t*>(&src);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) d[k] = s[k];
+    }
 
     // ---- event heap: SimKernel::schedule (event_queue.cpp:20-26) ----
     static DSD_HD bool key_less(int64_t ta, uint64_t ka, int64_t tb, uint64_t kb) {
@@ -431,9 +464,10 @@ struct Engine {
         int gamma;
     };
     DSD_HD Decision decide_window(int64_t i) {
-        int32_t d = draft_of(i);
+        const ReqRec& r = rec(i);
+        int32_t d = D > 0 ? r.drafter : -1;
         if (d < 0) return Decision{true, 1};
-        int32_t t = R[i].target;
+        int32_t t = r.target;
         switch (wkind()) {
             case 0:  // window_static (policies.cpp:55-58)
                 return Decision{false, gamma_s};
@@ -511,12 +545,12 @@ struct Engine {
     }
 
     // ---- work queues: intrusive lists through the records' item slots ----
-    DSD_HD int32_t slot_next(int32_t s) const { return R[s >> 1].next[s & 1]; }
-    DSD_HD void set_slot_next(int32_t s, int32_t n) { R[s >> 1].next[s & 1] = n; }
+    DSD_HD int32_t slot_next(int32_t s) const { return rec(s >> 1).next[s & 1]; }
+    DSD_HD void set_slot_next(int32_t s, int32_t n) { rec(s >> 1).next[s & 1] = n; }
 
     // push_work (engine.cpp:473-476): append, then try_dispatch as the next action
     DSD_HD void enqueue(int32_t v, int64_t i, int k, uint32_t op, int32_t tokens, bool via) {
-        ReqRec& r = R[i];
+        ReqRec& r = rec(i);
         r.op[k] = static_cast<uint8_t>(op | (via ? 4u : 0u));
         if (k) r.tok1 = tokens;
         r.enq[k] = now;
@@ -532,9 +566,9 @@ struct Engine {
         push_act(act(kActDispatch, static_cast<uint32_t>(v) * 2));
     }
 
-    DSD_HD bool eligible(bool is_draft, uint32_t op, int64_t req) const {
+    static DSD_HD bool eligible(bool is_draft, uint32_t op, const ReqRec& r) {
         // item_eligible (engine.cpp:478-483)
-        return is_draft || op == kOpPrefill || flag(req, kTpd);
+        return is_draft || op == kOpPrefill || flag(r, kTpd);
     }
 
     // try_dispatch (engine.cpp:485-567)
@@ -548,9 +582,10 @@ struct Engine {
         // eligible item of the single forming pass below.
         if (!is_draft && S.batching_window_us > 0 && !window_expired) {
             int64_t ncand = 0;
-            for (int32_t cur = SV(v_qhead, v); cur >= 0; cur = slot_next(cur)) {
-                uint32_t op = R[cur >> 1].op[cur & 1] & 3u;
-                if (!eligible(is_draft, op, cur >> 1)) continue;
+            for (int32_t cur = SV(v_qhead, v); cur >= 0; cur = rec(cur >> 1).next[cur & 1]) {
+                const ReqRec& rc = rec(cur >> 1);
+                uint32_t op = rc.op[cur & 1] & 3u;
+                if (!eligible(is_draft, op, rc)) continue;
                 if (kind < 0) kind = static_cast<int32_t>(op);
                 if (static_cast<int32_t>(op) != kind) continue;
                 ++ncand;
@@ -577,12 +612,12 @@ struct Engine {
         for (int32_t cur = SV(v_qhead, v); cur >= 0;) {
             const int64_t i = cur >> 1;
             const int k = cur & 1;
-            ReqRec& r = R[i];
+            ReqRec& r = rec(i);
             const int32_t nxt = r.next[k];
             const uint32_t opv = r.op[k];
             const uint32_t op = opv & 3u;
             bool take = false;
-            const bool elig = eligible(is_draft, op, i);
+            const bool elig = eligible(is_draft, op, r);
             if (elig && kind < 0) kind = static_cast<int32_t>(op);
             if (static_cast<int32_t>(op) == kind && elig) {
                 if (!lab) {  // batch_fifo (policies.cpp:30-38)
@@ -648,21 +683,21 @@ struct Engine {
     }
 
     // ---- request lifecycle ----
-    DSD_HD void record_gamma(int64_t i, int g) {
-        int32_t n = R[i].ng;
+    DSD_HD void record_gamma(ReqRec& r, int g) {
+        int32_t n = r.ng;
         if (W.collect) {
-            int64_t o = W.rep_seqbase[rep] + R[i].seqoff + n;
+            int64_t o = W.rep_seqbase[rep] + r.seqoff + n;
             if (o < W.seq_cap) W.seq_gamma[o] = g; else fail = kFailSeq;
         }
-        R[i].ng = n + 1;
+        r.ng = n + 1;
     }
-    DSD_HD void record_commit(int64_t i, int c) {
-        int32_t n = R[i].nc;
+    DSD_HD void record_commit(ReqRec& r, int c) {
+        int32_t n = r.nc;
         if (W.collect) {
-            int64_t o = W.rep_seqbase[rep] + R[i].seqoff + n;
+            int64_t o = W.rep_seqbase[rep] + r.seqoff + n;
             if (o < W.seq_cap) W.seq_commit[o] = c; else fail = kFailSeq;
         }
-        R[i].nc = n + 1;
+        r.nc = n + 1;
     }
 
     // activate_next_session (engine.cpp:332-339)
@@ -670,11 +705,13 @@ struct Engine {
         int32_t v = T + d;
         if (SV(v_active, v) >= 0 || SV(v_shead, v) < 0) return;
         int32_t i = SV(v_shead, v);
-        int32_t nx = R[i].snext;
+        const ReqRec& g = R[i];  // not active yet: the HBM record is current
+        int32_t nx = g.snext;
         SV(v_shead, v) = nx;
         if (nx < 0) SV(v_stail, v) = -1;
+        if (hotb) copy_rec(slot(d), g);
         SV(v_active, v) = i;
-        enqueue(v, i, 1, kOpPrefill, R[i].prompt, false);
+        enqueue(v, i, 1, kOpPrefill, g.prompt, false);
     }
 
     // route (engine.cpp:315-330, policies.cpp:9-28)
@@ -710,19 +747,21 @@ struct Engine {
 
     // on_arrival (engine.cpp:289-313)
     DSD_HD void on_arrival(int64_t i) {
-        set_phase(i, kPhRouted);
+        ReqRec& r = R[i];  // a new arrival is never an active session
+        set_phase(r, kPhRouted);
         int32_t t = route();
-        R[i].target = t;
+        r.target = t;
         ++SV(v_open, t);  // MetricsCollector::on_route
-        set_phase(i, kPhQueuedPrefill);
+        set_phase(r, kPhQueuedPrefill);
         if (fe()) {
-            set_flag(i, kFused, true);
-            enqueue(t, i, 0, kOpPrefill, R[i].prompt, false);
+            set_flag(r, kFused, true);
+            enqueue(t, i, 0, kOpPrefill, r.prompt, false);
         } else {
-            int32_t d = R[i].drafter;
+            int32_t d = r.drafter;
             int32_t v = T + d;
-            R[i].snext = -1;
+            r.snext = -1;
             int32_t tail = SV(v_stail, v);
+            // queued sessions are not active: their HBM records are current
             if (tail < 0) SV(v_shead, v) = static_cast<int32_t>(i); else R[tail].snext = static_cast<int32_t>(i);
             SV(v_stail, v) = static_cast<int32_t>(i);
             // activate_next_session runs first, then net_delay + schedule
@@ -734,39 +773,41 @@ struct Engine {
     // [decide_window] + begin_iteration (engine.cpp:254-257, 383-404)
     DSD_HD void begin(int64_t i, bool decide) {
         Decision dec = decide ? decide_window(i) : Decision{true, 1};
-        if (phase(i) == kPhDone) return;
-        int32_t d = draft_of(i);
-        int32_t t = R[i].target;
+        ReqRec& r = rec(i);
+        if (phase(r) == kPhDone) return;
+        int32_t d = D > 0 ? r.drafter : -1;
+        int32_t t = r.target;
         if (d >= 0 && t >= 0 && ps()) IL(W.p_gprev, W.c.np, pair_of(d, t)) = dec.fused ? 1 : dec.gamma;
         if (dec.fused) {
-            set_flag(i, kFused, true);
-            record_gamma(i, 0);
+            set_flag(r, kFused, true);
+            record_gamma(r, 0);
             enqueue(t, i, 1, kOpDecode, 1, false);
         } else {
-            set_flag(i, kFused, false);
-            record_gamma(i, dec.gamma);
-            R[i].pgamma = dec.gamma;
-            set_phase(i, kPhSpeculating);
+            set_flag(r, kFused, false);
+            record_gamma(r, dec.gamma);
+            r.pgamma = dec.gamma;
+            set_phase(r, kPhSpeculating);
             enqueue(T + d, i, 1, kOpDecode, dec.gamma, false);
         }
     }
 
     // finish_request (engine.cpp:449-468) + MetricsCollector::add_record
     DSD_HD void finish_request(int64_t i) {
-        ReqRec& r = R[i];
+        ReqRec& r = rec(i);
         r.done = now;
         if (r.first < 0) r.first = now;
-        set_phase(i, kPhDone);
+        set_phase(r, kPhDone);
         const int32_t t = r.target;
         --SV(v_open, t);
         if (r.output >= 2 && ps()) {
             double tpot = (static_cast<double>(now - r.first) / 1000.0) / static_cast<double>(r.output - 1);
             push_tpot(t, tpot);
         }
-        int32_t d = draft_of(i);
+        int32_t d = D > 0 ? r.drafter : -1;
         if (d >= 0) {
             int32_t v = T + d;
             if (SV(v_active, v) == static_cast<int32_t>(i)) {
+                if (hotb) copy_rec(R[i], slot(d));  // write the session back
                 SV(v_active, v) = -1;
                 push_act(act(kActActivate, static_cast<uint32_t>(d)));
             }
@@ -774,19 +815,17 @@ struct Engine {
     }
 
     // commit_tokens (engine.cpp:437-447); returns true when the request is done
-    DSD_HD bool commit_tokens(int64_t i, int32_t raw) {
-        ReqRec& r = R[i];
+    DSD_HD bool commit_tokens(ReqRec& r, int32_t raw) {
         int32_t remaining = r.output - r.tokens;
         int32_t c = raw < remaining ? raw : remaining;
         r.tokens += c;
-        record_commit(i, c);
+        record_commit(r, c);
         if (r.first < 0) r.first = now;
         return r.tokens >= r.output;
     }
 
     // consume_acceptance (engine.cpp:17-32) on the packed bits
-    DSD_HD void consume_acceptance(int64_t i, int gamma, int& accepted, int& consumed) {
-        ReqRec& r = R[i];
+    DSD_HD void consume_acceptance(ReqRec& r, int gamma, int& accepted, int& consumed) {
         const uint64_t* bits = W.bits + rep * W.c.bw + r.bitoff;
         const int32_t nb = r.nbits;
         int32_t cur = r.cursor;
@@ -809,16 +848,16 @@ struct Engine {
     DSD_HD void item_done(int32_t slot) {
         const int64_t i = slot >> 1;
         const int k = slot & 1;
-        ReqRec& r = R[i];
+        ReqRec& r = rec(i);
         const int32_t nxt = r.next[k];
         const uint32_t op = r.op[k] & 3u;
         if (nxt >= 0) push_act(act(kActItem, static_cast<uint32_t>(nxt)));
         if (item_server >= T) {  // draft server
             if (op == kOpPrefill) {
-                set_flag(i, kDpd, true);
+                set_flag(r, kDpd, true);
                 if (r.output > 0) schedule(now, info(kEvIterStart, 0, static_cast<uint32_t>(i)));
             } else {  // send_proposal (engine.cpp:591-597)
-                set_phase(i, kPhInFlightToTarget);
+                set_phase(r, kPhInFlightToTarget);
                 int64_t dl = net_delay(r.drafter, r.target);
                 r.outd = static_cast<int32_t>(dl);
                 schedule(now + dl, info(kEvNetArrive, kMsgProposal, static_cast<uint32_t>(i)));
@@ -826,28 +865,28 @@ struct Engine {
             return;
         }
         if (op == kOpPrefill) {
-            set_flag(i, kTpd, true);
+            set_flag(r, kTpd, true);
             if (r.output == 0) {
-                if (phase(i) != kPhDone) push_act(act(kActFinish, static_cast<uint32_t>(i)));
-            } else if (flag(i, kFused) && fe()) {
+                if (phase(r) != kPhDone) push_act(act(kActFinish, static_cast<uint32_t>(i)));
+            } else if (flag(r, kFused) && fe()) {
                 push_act(act(kActBegin, static_cast<uint32_t>(i) * 2));
             }
         } else if (op == kOpVerify) {
             int acc, cons;
-            consume_acceptance(i, r.tok1, acc, cons);
+            consume_acceptance(r, r.tok1, acc, cons);
             r.lcr = acc + 1;
             r.prop += cons;
             r.acc += acc;
             on_verify(r.drafter, r.target, cons, acc);
             int64_t bd = net_delay(r.drafter, r.target);
             r.backd = static_cast<int32_t>(bd);
-            set_phase(i, kPhInFlightToDraft);
+            set_phase(r, kPhInFlightToDraft);
             schedule(now + bd, info(kEvNetArrive, kMsgResult, static_cast<uint32_t>(i)));
         } else {  // fused decode step: commit one token, then the next iteration
-            if (commit_tokens(i, 1)) {
+            if (commit_tokens(r, 1)) {
                 push_act(act(kActFinish, static_cast<uint32_t>(i)));
             } else {
-                const bool decide = !(fe() || draft_of(i) < 0);
+                const bool decide = !(fe() || D == 0 || r.drafter < 0);
                 push_act(act(kActBegin, static_cast<uint32_t>(i) * 2 + (decide ? 1u : 0u)));
             }
         }
@@ -970,28 +1009,28 @@ struct Engine {
             case kActBegin: begin(arg >> 1, arg & 1u); break;
             case kActFinish: finish_request(arg); break;
             case kActSendPrompt: {
-                ReqRec& r = R[arg];
+                const ReqRec& r = rec(arg);
                 int64_t delay = net_delay(r.drafter, r.target);
                 schedule(now + delay, info(kEvNetArrive, kMsgPrompt, arg));
                 break;
             }
             case kActArrival: on_arrival(arg); break;
             case kActNetPrompt: {  // on_net_arrive (engine.cpp:406-435)
-                ReqRec& r = R[arg];
+                const ReqRec& r = rec(arg);
                 enqueue(r.target, arg, 0, kOpPrefill, r.prompt, true);
                 break;
             }
             case kActNetProposal: {
-                ReqRec& r = R[arg];
-                set_phase(arg, kPhVerifying);
+                ReqRec& r = rec(arg);
+                set_phase(r, kPhVerifying);
                 enqueue(r.target, arg, 1, kOpVerify, r.pgamma, true);
                 break;
             }
             case kActNetResult: {  // on_result_at_draft (engine.cpp:428-435)
-                ReqRec& r = R[arg];
+                ReqRec& r = rec(arg);
                 if (ps())
                     on_rtt_sample(r.drafter, r.target, static_cast<double>(static_cast<int64_t>(r.outd) + r.backd) / 1000.0);
-                if (commit_tokens(arg, r.lcr)) {
+                if (commit_tokens(r, r.lcr)) {
                     push_act(act(kActFinish, arg));
                 } else {
                     schedule(now, info(kEvIterStart, 0, arg));
@@ -1024,6 +1063,11 @@ struct Engine {
     // Engine::finish (engine.cpp:648-669) + aggregate_run (runner.cpp:153-169)
     DSD_HD void finish() {
         for (int32_t v = 0; v < T; ++v) IL(W.v_busy_us, W.c.ns, v) = get_busy(v);  // for the records export
+        if (hotb)  // sessions still active (a failed replica stops early): write them back
+            for (int32_t d = 0; d < D; ++d) {
+                const int32_t a = SV(v_active, T + d);
+                if (a >= 0) copy_rec(R[a], slot(d));
+            }
         DevSummary s;
         // every pop is one schedule() or one arrival (event_queue.cpp:38):
         // arrivals popped + dynamic events scheduled - still pending

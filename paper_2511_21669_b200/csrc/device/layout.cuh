@@ -123,7 +123,10 @@ struct DevRecord {  // == dsd_request_record
 // Work-item slot k of request i has id 2*i + k: k = 0 is the target prefill
 // item, k = 1 is the request's other item (draft prefill / draft decode /
 // verify / fused decode); a request never has two items of the same slot.
-struct alignas(128) ReqRec {
+// Records are 128-byte aligned in HBM (one line each); the shared-memory
+// copies of active sessions (Engine::rec) sit at a kHotStride lane stride,
+// so the struct itself only asks for 8-byte alignment.
+struct ReqRec {
     int64_t arrival;       // arrival event time (trace or re-sampled)
     int64_t first;         // first-token time, -1 before the first commit
     int64_t done;          // completion time, -1 while running
@@ -144,6 +147,7 @@ struct alignas(128) ReqRec {
     uint8_t pad;
 };
 static_assert(sizeof(ReqRec) == 128, "request record must be one 128-byte line");
+constexpr int kHotStride = 136;  // 34 words: at most 2-way bank conflicts, 8-byte aligned
 
 struct Workspace {
     Caps c;

@@ -75,6 +75,13 @@ __global__ void __launch_bounds__(kBlock) k_stage(Workspace W, int64_t* ltot, co
 //
 // __launch_bounds__(64, 8): <= 128 registers, so 8 blocks (16 warps) fit per
 // SM and a 65,536-replica sweep (13.8 warps/SM on 148 SMs) is one wave.
+// Shared memory per warp of the kSmem variant: server fields, heap slots and
+// the active-session record slots (one per possible draft server, ns - 1).
+__host__ __device__ inline int64_t smem_warp_bytes(int64_t ns, int64_t heap_cap) {
+    return static_cast<int64_t>(kServerFields) * ns * kLanes * 4 + heap_cap * kLanes * 16 +
+           (ns - 1) * kLanes * kHotStride;
+}
+
 template <bool kSmem, bool kStats>
 __global__ void __launch_bounds__(kBlock, 8) k_simulate(Workspace W, const int32_t* list, const int32_t* count,
                                                      int32_t smem_heap_cap) {
@@ -86,16 +93,18 @@ __global__ void __launch_bounds__(kBlock, 8) k_simulate(Workspace W, const int32
     uint64_t* kb;
     int64_t hcap;
     int32_t nsc;
+    unsigned char* hot = nullptr;
     if constexpr (kSmem) {
         extern __shared__ __align__(16) unsigned char smem[];
         const int lane = threadIdx.x % kLanes;
         nsc = static_cast<int32_t>(W.c.ns);
         hcap = smem_heap_cap;
         const int64_t srv_bytes = static_cast<int64_t>(kServerFields) * nsc * kLanes * 4;
-        unsigned char* blk = smem + (threadIdx.x / kLanes) * (srv_bytes + hcap * kLanes * 16);
+        unsigned char* blk = smem + (threadIdx.x / kLanes) * smem_warp_bytes(nsc, hcap);
         sbase = reinterpret_cast<int32_t*>(blk) + lane;
         hb = reinterpret_cast<int64_t*>(blk + srv_bytes) + lane;
         kb = reinterpret_cast<uint64_t*>(blk + srv_bytes + hcap * kLanes * 8) + lane;
+        hot = blk + srv_bytes + hcap * kLanes * 16 + lane * kHotStride;
     } else {
         const int64_t w = r / kLanes, lane = r % kLanes;
         nsc = static_cast<int32_t>(W.c.ns);
@@ -104,7 +113,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_simulate(Workspace W, const int32
         hb = W.h_time + w * W.c.hc * kLanes + lane;
         kb = W.h_key + w * W.c.hc * kLanes + lane;
     }
-    Engine e(W, W.scen[W.rep_scen[r]], r, sbase, hb, kb, hcap, nsc);
+    Engine e(W, W.scen[W.rep_scen[r]], r, sbase, hb, kb, hcap, nsc, hot);
     if (live) e.init();
     uint32_t kind = live ? e.next_kind() : static_cast<uint32_t>(kActNone);
     // kStats: per-step-kind cycle profile (DSD_STEP_STATS=1), one block-level
@@ -375,9 +384,7 @@ void Runtime::launch() {
     DSD_CUDA(cudaEventRecord(R.ev[1], R.stream));
     const bool smem = R.W.c.ns <= kSmemServers && R.smem_heap > 0;
     if (smem) {
-        const size_t bytes = static_cast<size_t>(kBlock / kLanes) *
-                             (static_cast<size_t>(kServerFields) * R.W.c.ns * kLanes * 4 +
-                              static_cast<size_t>(R.smem_heap) * kLanes * 16);
+        const size_t bytes = static_cast<size_t>(kBlock / kLanes) * smem_warp_bytes(R.W.c.ns, R.smem_heap);
         (R.step_stats ? k_simulate<true, true> : k_simulate<true, false>)<<<grid, kBlock, bytes, R.stream>>>(R.W, nullptr, nullptr, R.smem_heap);
         DSD_CUDA(cudaGetLastError());
         // replicas whose event heap outgrew shared memory run again from HBM

@@ -1,0 +1,10 @@
+# quick GPU check: C5 timing (A/B against build/ab/base.so when present), the
+# lone-warp gamma=1 subset, then the GPU parity suite
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+for i in 1 2; do
+  if [ -f build/ab/base.so ]; then echo -n "base "; DSD_LIB=$PWD/build/ab/base.so python tools/profile_sweep.py --launches 3 2>&1 | tail -2 | head -1; fi
+  echo -n "cur  "; python tools/profile_sweep.py --launches 3 2>&1 | tail -2 | head -1
+done
+if [ -f build/ab/sub_g1.yaml ]; then echo -n "lone g1 "; python tools/profile_sweep.py --spec build/ab/sub_g1.yaml --launches 2 2>&1 | tail -2 | head -1; fi
+python -m pytest tests -q -x -m gpu ${PYTEST_ARGS:-} 2>&1 | tail -3
