@@ -213,6 +213,10 @@ struct Engine {
     uint32_t st0 = 0, st1 = 0, st2 = 0, st3 = 0;
     int32_t sp = 0;
     int32_t item_server = -1;
+    // the one event a step schedules (pend_t < 0: none); step() inserts it
+    // at its end, so the heap insertion is inlined once
+    int64_t pend_t = -1;
+    uint32_t pend_info = 0;
     // per-warp state blocks (shared memory for small topologies, else HBM),
     // already offset by this lane: element k of a field is at base[k * 32]
     int32_t* sb;     // server fields [kServerFields][nsc]
@@ -259,7 +263,8 @@ struct Engine {
         F_v_open, F_v_busy_lo, F_v_busy_hi
     };
 #define SV(field, i) sv(F_##field, (i))
-    DSD_HD int32_t& sv(int f, int32_t v) const { return sb[(static_cast<int64_t>(f) * nsc + v) * kLanes]; }
+    // (32-bit index math: server and heap blocks are far below 2^31 elements)
+    DSD_HD int32_t& sv(int f, int32_t v) const { return sb[(f * nsc + v) * kLanes]; }
     // Server::busy_us (engine.cpp:562) as two 32-bit halves in the server block
     DSD_HD int64_t get_busy(int32_t v) const {
         return static_cast<int64_t>((static_cast<uint64_t>(static_cast<uint32_t>(SV(v_busy_hi, v))) << 32) |
@@ -269,8 +274,8 @@ struct Engine {
         SV(v_busy_lo, v) = static_cast<int32_t>(static_cast<uint32_t>(x));
         SV(v_busy_hi, v) = static_cast<int32_t>(static_cast<uint32_t>(static_cast<uint64_t>(x) >> 32));
     }
-    DSD_HD int64_t& ht(int64_t k) const { return htb[k * kLanes]; }
-    DSD_HD uint64_t& hk(int64_t k) const { return hkb[k * kLanes]; }
+    DSD_HD int64_t& ht(int32_t k) const { return htb[k * kLanes]; }
+    DSD_HD uint64_t& hk(int32_t k) const { return hkb[k * kLanes]; }
 
     // ---- action stack ----
     static DSD_HD uint32_t act(uint32_t kind, uint32_t arg) { return kind | (arg << 4); }
@@ -284,24 +289,6 @@ struct Engine {
         st1 = st0;
         st0 = a;
         ++sp;
-        // the action runs a few warp iterations later: start pulling its
-        // request record into L1 now
-        const uint32_t k = a & 15u, arg = a >> 4;
-        if ((k >= kActArrival && k <= kActNetResult) || k == kActFinish || k == kActSendPrompt) {
-            prefetch_record(arg);
-        } else if (k == kActBegin || k == kActItem) {
-            prefetch_record(arg >> 1);
-        }
-    }
-    DSD_HD void prefetch_record(uint32_t i) const {
-#ifdef __CUDA_ARCH__
-        if (hotb)  // an active session lives in shared memory
-            for (int32_t d = 0; d < D; ++d)
-                if (SV(v_active, T + d) == static_cast<int32_t>(i)) return;
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(R + i));
-#else
-        (void)i;
-#endif
     }
     DSD_HD uint32_t pop_act() {
         uint32_t a = st0;
@@ -352,6 +339,10 @@ struct Engine {
     static DSD_HD bool key_less(int64_t ta, uint64_t ka, int64_t tb, uint64_t kb) {
         return ta < tb || (ta == tb && ka < kb);
     }
+    DSD_HD void defer(int64_t t, uint32_t inf) {
+        pend_t = t;
+        pend_info = inf;
+    }
     DSD_HD void schedule(int64_t t, uint32_t info) {
         if (heap_n >= hcap) {
             fail = kFailHeap;
@@ -359,9 +350,9 @@ struct Engine {
         }
         uint64_t key = (static_cast<uint64_t>(seq_next) << 32) | info;
         ++seq_next;
-        int64_t i = heap_n++;
+        int32_t i = heap_n++;
         while (i > 0) {
-            int64_t p = (i - 1) >> 1;
+            int32_t p = (i - 1) >> 1;
             int64_t pt = ht(p);
             uint64_t pk = hk(p);
             if (!key_less(t, key, pt, pk)) break;
@@ -373,13 +364,13 @@ struct Engine {
         hk(i) = key;
     }
     DSD_HD void heap_pop() {
-        int64_t n = --heap_n;
+        int32_t n = --heap_n;
         if (n == 0) return;
         int64_t t = ht(n);
         uint64_t k = hk(n);
-        int64_t i = 0;
+        int32_t i = 0;
         for (;;) {
-            int64_t c = 2 * i + 1;
+            int32_t c = 2 * i + 1;
             if (c >= n) break;
             int64_t ct = ht(c);
             uint64_t ck = hk(c);
@@ -595,7 +586,7 @@ struct Engine {
                 if (!SV(v_armed, v)) {
                     SV(v_armed, v) = 1;
                     SV(v_armseq, v) = seq_next;  // stands in for ++window_gen (engine.cpp:512-517)
-                    schedule(now + S.batching_window_us, info(kEvBatchReady, 0, static_cast<uint32_t>(v)));
+                    defer(now + S.batching_window_us, info(kEvBatchReady, 0, static_cast<uint32_t>(v)));
                 }
                 return;
             }
@@ -679,7 +670,7 @@ struct Engine {
         if (lat < 1) lat = 1;
         SV(v_busy, v) = 1;
         set_busy(v, get_busy(v) + lat);
-        schedule(now + lat, info(kEvComputeDone, 0, static_cast<uint32_t>(v)));
+        defer(now + lat, info(kEvComputeDone, 0, static_cast<uint32_t>(v)));
     }
 
     // ---- request lifecycle ----
@@ -855,12 +846,12 @@ struct Engine {
         if (item_server >= T) {  // draft server
             if (op == kOpPrefill) {
                 set_flag(r, kDpd, true);
-                if (r.output > 0) schedule(now, info(kEvIterStart, 0, static_cast<uint32_t>(i)));
+                if (r.output > 0) defer(now, info(kEvIterStart, 0, static_cast<uint32_t>(i)));
             } else {  // send_proposal (engine.cpp:591-597)
                 set_phase(r, kPhInFlightToTarget);
                 int64_t dl = net_delay(r.drafter, r.target);
                 r.outd = static_cast<int32_t>(dl);
-                schedule(now + dl, info(kEvNetArrive, kMsgProposal, static_cast<uint32_t>(i)));
+                defer(now + dl, info(kEvNetArrive, kMsgProposal, static_cast<uint32_t>(i)));
             }
             return;
         }
@@ -881,7 +872,7 @@ struct Engine {
             int64_t bd = net_delay(r.drafter, r.target);
             r.backd = static_cast<int32_t>(bd);
             set_phase(r, kPhInFlightToDraft);
-            schedule(now + bd, info(kEvNetArrive, kMsgResult, static_cast<uint32_t>(i)));
+            defer(now + bd, info(kEvNetArrive, kMsgResult, static_cast<uint32_t>(i)));
         } else {  // fused decode step: commit one token, then the next iteration
             if (commit_tokens(r, 1)) {
                 push_act(act(kActFinish, static_cast<uint32_t>(i)));
@@ -1011,7 +1002,7 @@ struct Engine {
             case kActSendPrompt: {
                 const ReqRec& r = rec(arg);
                 int64_t delay = net_delay(r.drafter, r.target);
-                schedule(now + delay, info(kEvNetArrive, kMsgPrompt, arg));
+                defer(now + delay, info(kEvNetArrive, kMsgPrompt, arg));
                 break;
             }
             case kActArrival: on_arrival(arg); break;
@@ -1033,7 +1024,7 @@ struct Engine {
                 if (commit_tokens(r, r.lcr)) {
                     push_act(act(kActFinish, arg));
                 } else {
-                    schedule(now, info(kEvIterStart, 0, arg));
+                    defer(now, info(kEvIterStart, 0, arg));
                 }
                 break;
             }
@@ -1049,6 +1040,10 @@ struct Engine {
                 }
                 break;
             }
+        }
+        if (pend_t >= 0) {
+            schedule(pend_t, pend_info);
+            pend_t = -1;
         }
     }
 
