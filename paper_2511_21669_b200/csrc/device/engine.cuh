@@ -72,7 +72,8 @@ DSD_HD double grid_interpolate_int(const char* blob, const DevGrid& g, int64_t q
     return r * g.calibration;
 }
 
-DSD_HD double grid_interpolate(const char* blob, const DevGrid& g, double batch, double context) {
+// General (non-integer or table-less) query; out of line, it is cold.
+DSD_HD_NOINLINE double grid_interpolate(const char* blob, const DevGrid& g, double batch, double context) {
     const double* ba = blob_ptr<double>(blob, g.o_batch);
     const double* ca = blob_ptr<double>(blob, g.o_ctx);
     const double* v = blob_ptr<double>(blob, g.o_vals);
@@ -328,7 +329,8 @@ struct Engine {
         }
         return R[i];
     }
-    static DSD_HD void copy_rec(ReqRec& dst, const ReqRec& src) {
+    // out of line: runs twice per request (activation, write-back)
+    static DSD_HD_NOINLINE void copy_rec(ReqRec& dst, const ReqRec& src) {
         uint64_t* d = reinterpret_cast<uint64_t*>(&dst);
         const uint64_t* s = reinterpret_cast<const uint64_t*>(&src);
 #pragma unroll
