@@ -205,6 +205,7 @@ struct Engine {
     uint32_t seq_next;  // next seq for schedule(); arrivals hold 0..N-1
     int32_t heap_n = 0;
     int32_t next_arr = 0;
+    int64_t next_arr_t = 0;  // arrival time of arrival next_arr (valid while next_arr < N)
     Rng jitter;
     int64_t net_wait_total = 0;
     int32_t net_wait_count = 0;
@@ -226,7 +227,9 @@ struct Engine {
     int32_t hcap;
     int32_t nsc;
     // hot scenario parameters: packed policy flags + the static window
-    uint32_t pflags;  // fused_everything | pair_stats<<1 | lab<<2 | jitter_free<<3 | window<<4 | routing<<6
+    // fused_everything | pair_stats<<1 | lab<<2 | jitter_free<<3 | window<<4 | routing<<6 |
+    // has_order<<8 | single_link<<9 | batching_window<<10
+    uint32_t pflags;
     int32_t gamma_s, max_batch, dmax_batch;
 
     DSD_HD Engine(const Workspace& w, const DevScenario& s, int64_t replica, int32_t* server_base,
@@ -240,7 +243,10 @@ struct Engine {
         hotb = S.fused_everything ? nullptr : hot_base;
         pflags = static_cast<uint32_t>(S.fused_everything) | (static_cast<uint32_t>(S.pair_stats) << 1) |
                  (static_cast<uint32_t>(S.batching == 1) << 2) | (static_cast<uint32_t>(S.jitter_free) << 3) |
-                 (static_cast<uint32_t>(S.window_kind) << 4) | (static_cast<uint32_t>(S.routing) << 6);
+                 (static_cast<uint32_t>(S.window_kind) << 4) | (static_cast<uint32_t>(S.routing) << 6) |
+                 (static_cast<uint32_t>(S.has_order != 0) << 8) |
+                 (static_cast<uint32_t>(S.n_dg == 1 && S.n_tg == 1) << 9) |
+                 (static_cast<uint32_t>(S.batching_window_us > 0) << 10);
         gamma_s = S.gamma;
         max_batch = S.max_batch;
         dmax_batch = S.draft_max_batch;
@@ -251,6 +257,9 @@ struct Engine {
     DSD_HD bool jitter_free() const { return (pflags >> 3) & 1u; }
     DSD_HD uint32_t wkind() const { return (pflags >> 4) & 3u; }
     DSD_HD uint32_t routing_kind() const { return (pflags >> 6) & 3u; }
+    DSD_HD bool has_order() const { return (pflags >> 8) & 1u; }
+    DSD_HD bool single_link() const { return (pflags >> 9) & 1u; }
+    DSD_HD bool batching_window() const { return (pflags >> 10) & 1u; }
     // warp-interleaved per-replica arrays in HBM (pair stats, busy export)
     template <typename U>
     DSD_HD U& IL(U* base, int64_t cap, int64_t idx) const {
@@ -258,10 +267,16 @@ struct Engine {
     }
 
     // server fields (engine.cpp:70-84 Server, minus the queue/running vectors
-    // which are intrusive lists through the request records)
+    // which are intrusive lists through the request records).  Targets and
+    // draft servers use disjoint fields, overlaid: targets keep the batching
+    // window's arm sequence, open requests and busy time (only target busy
+    // time is reported); draft servers keep the active session and the
+    // session FIFO.
     enum : int {
-        F_v_qhead = 0, F_v_qtail, F_v_run, F_v_busy, F_v_armed, F_v_armseq, F_v_active, F_v_shead, F_v_stail,
-        F_v_open, F_v_busy_lo, F_v_busy_hi
+        F_v_qhead = 0, F_v_qtail = 1, F_v_run = 2,
+        F_v_flags = 3,  // busy | armed << 1
+        F_v_armseq = 4, F_v_open = 5, F_v_busy_lo = 6, F_v_busy_hi = 7,  // targets
+        F_v_active = 4, F_v_shead = 5, F_v_stail = 6                      // draft servers
     };
 #define SV(field, i) sv(F_##field, (i))
     // (32-bit index math: server and heap blocks are far below 2^31 elements)
@@ -275,6 +290,10 @@ struct Engine {
         SV(v_busy_lo, v) = static_cast<int32_t>(static_cast<uint32_t>(x));
         SV(v_busy_hi, v) = static_cast<int32_t>(static_cast<uint32_t>(static_cast<uint64_t>(x) >> 32));
     }
+    DSD_HD bool busy(int32_t v) const { return SV(v_flags, v) & 1; }
+    DSD_HD bool armed(int32_t v) const { return SV(v_flags, v) & 2; }
+    DSD_HD void set_busy_flag(int32_t v, bool b) { SV(v_flags, v) = (SV(v_flags, v) & ~1) | (b ? 1 : 0); }
+    DSD_HD void set_armed(int32_t v, bool b) { SV(v_flags, v) = (SV(v_flags, v) & ~2) | (b ? 2 : 0); }
     DSD_HD int64_t& ht(int32_t k) const { return htb[k * kLanes]; }
     DSD_HD uint64_t& hk(int32_t k) const { return hkb[k * kLanes]; }
 
@@ -321,6 +340,13 @@ struct Engine {
     // touches a record; the slot is authoritative while i is active.
     DSD_HD ReqRec& slot(int32_t d) const {
         return *reinterpret_cast<ReqRec*>(hotb + static_cast<int64_t>(d) * kLanes * kHotStride);
+    }
+    // the first kHotBitWords acceptance-bit words of draft d's active session,
+    // lane-interleaved after the session slots (word k at [k * kLanes])
+    DSD_HD uint64_t* hot_bits(int32_t d) const {
+        const int lane = rep & 31;
+        unsigned char* base = hotb - lane * kHotStride + static_cast<int64_t>(nsc - 1) * kLanes * kHotStride;
+        return reinterpret_cast<uint64_t*>(base) + lane + d * kHotBitWords * kLanes;
     }
     DSD_HD ReqRec& rec(int64_t i) const {
         if (hotb) {
@@ -398,7 +424,7 @@ struct Engine {
     // ---- network: net_delay (engine.cpp:10-15) ----
     DSD_HD const DevLink& link(int32_t d, int32_t t) const {
         const DevLink* links = blob_ptr<DevLink>(W.blob, S.o_links);
-        if (S.n_dg == 1 && S.n_tg == 1) return links[0];
+        if (single_link()) return links[0];
         const int32_t* dg = blob_ptr<int32_t>(W.blob, S.o_dgroup);
         const int32_t* tg = blob_ptr<int32_t>(W.blob, S.o_tgroup);
         return links[dg[d] * S.n_tg + tg[t]];
@@ -566,14 +592,14 @@ struct Engine {
 
     // try_dispatch (engine.cpp:485-567)
     DSD_HD void try_dispatch(int32_t v, bool window_expired) {
-        if (SV(v_busy, v) || SV(v_qhead, v) < 0) return;
+        if (busy(v) || SV(v_qhead, v) < 0) return;
         const bool is_draft = v >= T;
         const int64_t mb = is_draft ? dmax_batch : max_batch;
         int32_t kind = -1;
         // Only an armable batching window needs the candidate count before
         // anything is taken; otherwise the head kind is fixed by the first
         // eligible item of the single forming pass below.
-        if (!is_draft && S.batching_window_us > 0 && !window_expired) {
+        if (!is_draft && batching_window() && !window_expired) {
             int64_t ncand = 0;
             for (int32_t cur = SV(v_qhead, v); cur >= 0; cur = rec(cur >> 1).next[cur & 1]) {
                 const ReqRec& rc = rec(cur >> 1);
@@ -585,14 +611,14 @@ struct Engine {
             }
             if (ncand == 0) return;
             if (ncand < mb) {
-                if (!SV(v_armed, v)) {
-                    SV(v_armed, v) = 1;
+                if (!armed(v)) {
+                    set_armed(v, true);
                     SV(v_armseq, v) = seq_next;  // stands in for ++window_gen (engine.cpp:512-517)
                     defer(now + S.batching_window_us, info(kEvBatchReady, 0, static_cast<uint32_t>(v)));
                 }
                 return;
             }
-            SV(v_armed, v) = 0;
+            set_armed(v, false);
         }
 
         const bool lab = !is_draft && lab_batching();
@@ -670,8 +696,8 @@ struct Engine {
         if (decode) ms *= tok;
         int64_t lat = llround(ms * 1000.0);
         if (lat < 1) lat = 1;
-        SV(v_busy, v) = 1;
-        set_busy(v, get_busy(v) + lat);
+        set_busy_flag(v, true);
+        if (!is_draft) set_busy(v, get_busy(v) + lat);  // only target busy time is reported
         defer(now + lat, info(kEvComputeDone, 0, static_cast<uint32_t>(v)));
     }
 
@@ -819,7 +845,7 @@ struct Engine {
 
     // consume_acceptance (engine.cpp:17-32) on the packed bits
     DSD_HD void consume_acceptance(ReqRec& r, int gamma, int& accepted, int& consumed) {
-        const uint64_t* bits = W.bits + rep * W.c.bw + r.bitoff;
+        const uint64_t* bits = W.bits + static_cast<int64_t>(rep) * W.c.bw + r.bitoff;
         const int32_t nb = r.nbits;
         int32_t cur = r.cursor;
         accepted = 0;
@@ -901,18 +927,21 @@ struct Engine {
         jitter.seed(seed, kLabelJitter);
         N = (S.workload == 0) ? S.n_requests : S.tr_n;
         seq_next = static_cast<uint32_t>(N);
+        if (N > 0) next_arr_t = R[arrival_index(0)].arrival;
         for (int32_t v = 0; v < T + D; ++v) {
             SV(v_qhead, v) = -1;
             SV(v_qtail, v) = -1;
             SV(v_run, v) = -1;
-            SV(v_busy, v) = 0;
-            SV(v_armed, v) = 0;
-            SV(v_armseq, v) = 0;
-            set_busy(v, 0);
-            SV(v_active, v) = -1;
-            SV(v_shead, v) = -1;
-            SV(v_stail, v) = -1;
-            SV(v_open, v) = 0;
+            SV(v_flags, v) = 0;
+            if (v < T) {
+                SV(v_armseq, v) = 0;
+                SV(v_open, v) = 0;
+                set_busy(v, 0);
+            } else {
+                SV(v_active, v) = -1;
+                SV(v_shead, v) = -1;
+                SV(v_stail, v) = -1;
+            }
         }
         if (ps()) {
             for (int32_t t = 0; t < T; ++t) {
@@ -936,7 +965,7 @@ struct Engine {
     }
 
     DSD_HD int64_t arrival_index(int64_t k) const {
-        if (S.has_order) return blob_ptr<int64_t>(W.blob, S.o_tr_order)[k];
+        if (has_order()) return blob_ptr<int64_t>(W.blob, S.o_tr_order)[k];
         return k;
     }
 
@@ -953,14 +982,13 @@ struct Engine {
     // The event's handler becomes the next action.
     DSD_HD void pop_event() {
         const bool have_arr = next_arr < N;
-        int64_t ai = 0, ta = 0;
-        if (have_arr) {
-            ai = arrival_index(next_arr);
-            ta = R[ai].arrival;
-        }
-        if (have_arr && (heap_n == 0 || ta <= ht(0))) {
+        if (have_arr && (heap_n == 0 || next_arr_t <= ht(0))) {
+            const int64_t ai = arrival_index(next_arr);
+            now = next_arr_t;
             ++next_arr;
-            now = ta;
+            // the following arrival's time: not needed before the next pop,
+            // so the load's latency hides behind this event
+            if (next_arr < N) next_arr_t = R[arrival_index(next_arr)].arrival;
             push_act(act(kActArrival, static_cast<uint32_t>(ai)));
             return;
         }
@@ -980,8 +1008,8 @@ struct Engine {
             push_act(act(kActComputeDone, id));
         } else if (kind == kEvBatchReady) {  // engine.cpp:265-271
             const int32_t v = static_cast<int32_t>(id);
-            if (SV(v_armed, v) && SV(v_armseq, v) == static_cast<uint32_t>(key >> 32)) {
-                SV(v_armed, v) = 0;
+            if (armed(v) && SV(v_armseq, v) == static_cast<uint32_t>(key >> 32)) {
+                set_armed(v, false);
                 push_act(act(kActDispatch, static_cast<uint32_t>(v) * 2 + 1));
             }
         }
@@ -1032,7 +1060,7 @@ struct Engine {
             }
             default: {  // kActComputeDone: on_compute_done (engine.cpp:569-589)
                 const int32_t v = static_cast<int32_t>(arg);
-                SV(v_busy, v) = 0;
+                set_busy_flag(v, false);
                 const int32_t head = SV(v_run, v);
                 SV(v_run, v) = -1;
                 push_act(act(kActDispatch, static_cast<uint32_t>(v) * 2));

@@ -16,13 +16,15 @@ namespace dsd {
 
 constexpr int kLanes = 32;
 constexpr int kMaxHidden = 64;  // AWC hidden width supported by the engine
-constexpr int kServerFields = 12;
-// Shared-memory variant of the simulation kernel: per-warp server state and a
-// heap of kSmemHeap slots live in shared memory; a replica whose dynamic event
-// heap outgrows it is re-run on the HBM variant.
+// int32 fields per server (Engine::F_*; targets and draft servers use
+// disjoint subsets, overlaid)
+constexpr int kServerFields = 8;
+// Shared-memory variant of the simulation kernel (<= kSmemServers servers):
+// per-warp server state, the first heap slots and the draft servers' active
+// sessions live in shared memory; a replica whose dynamic event heap outgrows
+// it is re-run on the HBM variant.
 constexpr int kSmemServers = 4;
-constexpr int kSmemHeap = 24;
-constexpr int kSmemWarpBytes = kServerFields * kSmemServers * kLanes * 4 + kSmemHeap * kLanes * 16;
+constexpr int kHotBitWords = 4;  // acceptance-bit words of an active session kept in shared memory
 
 // Event kinds (proj/include/specsim/sim/event_queue.hpp:12-18).
 enum : uint32_t { kEvArrival = 0, kEvBatchReady = 1, kEvComputeDone = 2, kEvNetArrive = 3, kEvIterStart = 4 };

@@ -75,8 +75,9 @@ __global__ void __launch_bounds__(kBlock) k_stage(Workspace W, int64_t* ltot, co
 //
 // __launch_bounds__(64, 8): <= 128 registers, so 8 blocks (16 warps) fit per
 // SM and a 65,536-replica sweep (13.8 warps/SM on 148 SMs) is one wave.
-// Shared memory per warp of the kSmem variant: server fields, heap slots and
-// the active-session record slots (one per possible draft server, ns - 1).
+// Shared memory per warp of the kSmem variant: server fields, heap slots, the
+// active-session record slots (one per possible draft server, ns - 1) and
+// their first acceptance-bit words.
 __host__ __device__ inline int64_t smem_warp_bytes(int64_t ns, int64_t heap_cap) {
     return static_cast<int64_t>(kServerFields) * ns * kLanes * 4 + heap_cap * kLanes * 16 +
            (ns - 1) * kLanes * kHotStride;
@@ -223,7 +224,9 @@ struct RuntimeImpl {
     DevBuf blob, scen, reps, arena, summary, fail, ltot, seqbase, seqg, seqc, rec, busy, ovf;
     // shared-memory heap slots per replica for small topologies (0 = always
     // run the HBM variant; env DSD_SMEM_HEAP overrides, for tests)
-    int32_t smem_heap = 8;
+    // 7: with 8 server fields x 2 servers and one session slot a warp needs
+    // 9.75 KB, so 8 blocks/SM fit the 164 KB carveout (L1 keeps 92 KB)
+    int32_t smem_heap = 7;
     bool step_stats = false;  // env DSD_STEP_STATS=1: per-step-kind cycle profile to stderr
     DevBuf stats;
     Workspace W{};
