@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <numeric>
 #include <string>
 #include <type_traits>
@@ -19,7 +20,7 @@ namespace {
 
 struct BlobBuilder {
     std::vector<char> data;
-    std::map<const void*, int64_t> seen;
+    std::unordered_map<const void*, int64_t> seen;
     int64_t put(const void* src, size_t bytes, bool dedupe = true) {
         if (dedupe && src) {
             auto it = seen.find(src);
@@ -74,6 +75,8 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
     if (ns == 0 && n > 0) cfg_error("batch has replicas but no scenarios");
     Packed P;
     BlobBuilder B;
+    B.data.reserve(256 * ns + (1u << 16));
+    B.seen.reserve(8 * ns);
     std::vector<DevScenario>& ds = P.scen;
     ds.resize(ns);
     Caps& c = P.caps;
@@ -85,11 +88,12 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
         const dsd_scenario& s = sc[k];
         DevScenario& d = ds[k];
         std::memset(&d, 0, sizeof(d));
-        const std::string where = "scenario " + std::to_string(k) + ": ";
-        if (s.n_targets < 1) cfg_error(where + "target pool must be non-empty");
-        if (s.n_drafts < 0) cfg_error(where + "negative draft pool");
+        // error-message prefix, built only when a check fails
+        const auto where = [k] { return "scenario " + std::to_string(k) + ": "; };
+        if (s.n_targets < 1) cfg_error(where() + "target pool must be non-empty");
+        if (s.n_drafts < 0) cfg_error(where() + "negative draft pool");
         if (s.n_target_groups < 1 || (s.n_drafts > 0 && s.n_draft_groups < 1))
-            cfg_error(where + "group counts must be >= 1");
+            cfg_error(where() + "group counts must be >= 1");
         d.n_targets = s.n_targets;
         d.n_drafts = s.n_drafts;
         d.n_tg = s.n_target_groups;
@@ -97,15 +101,15 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
         d.fused_everything = (s.window_kind == DSD_WINDOW_FUSED || s.n_drafts == 0) ? 1 : 0;
         for (int i = 0; i < s.n_targets; ++i)
             if (s.target_group[i] < 0 || s.target_group[i] >= s.n_target_groups)
-                cfg_error(where + "target group out of range");
+                cfg_error(where() + "target group out of range");
         for (int i = 0; i < s.n_drafts; ++i)
             if (s.draft_group[i] < 0 || s.draft_group[i] >= s.n_draft_groups)
-                cfg_error(where + "draft group out of range");
+                cfg_error(where() + "draft group out of range");
         int32_t zero = 0;
         d.o_tgroup = B.put(s.target_group, sizeof(int32_t) * s.n_targets);
         d.o_dgroup = s.n_drafts > 0 ? B.put(s.draft_group, sizeof(int32_t) * s.n_drafts)
                                     : B.put(&zero, sizeof(zero), false);
-        if (!s.links) cfg_error(where + "missing link table");
+        if (!s.links) cfg_error(where() + "missing link table");
         {
             size_t nl = static_cast<size_t>(d.n_dg) * d.n_tg;
             for (size_t l = 0; l < nl; ++l) {
@@ -135,7 +139,7 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
             d.jitter_free = jitter_free ? 1 : 0;
         }
         // grids
-        if (s.n_grids < 1 || !s.grids) cfg_error(where + "latency profile has no grids");
+        if (s.n_grids < 1 || !s.grids) cfg_error(where() + "latency profile has no grids");
         auto git = grid_tables.find(s.grids);
         if (git == grid_tables.end()) {
             std::vector<DevGrid> g(s.n_grids);

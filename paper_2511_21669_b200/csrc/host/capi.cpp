@@ -5,6 +5,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 
 #include "../device/runtime.hpp"
 #include "dsdsim.h"
@@ -195,11 +196,21 @@ int dsd_run_sweep(dsd_handle* h, const char* sweep_yaml, const char* base_dir, c
                   char** summary_json, char** summary_csv, double* totals, char* err, size_t errlen) {
     return guard(err, errlen, [&] {
         need(h);
+        dsd::host::PhaseTimer tm("dsd_run_sweep");
         dsd::cfg::Node node = dsd::cfg::parse(sweep_yaml ? sweep_yaml : "");
+        tm.lap("parse");
         dsd::host::SweepBatch b = dsd::host::plan_sweep(node, base_dir ? base_dir : ".", 0, 1, &h->caches);
+        tm.lap("plan");
         dsd::host::SweepTotals t = dsd::host::run_sweep(*h->rt, b, out_dir ? out_dir : "");
+        tm.lap("run");
+        // the two summary texts are independent: build the CSV alongside the JSON
+        std::string csv;
+        std::thread csv_thread;
+        if (summary_csv) csv_thread = std::thread([&] { csv = dsd::host::sweep_summary_csv(b.points); });
         if (summary_json) *summary_json = dup(dsd::host::sweep_summary_json(b.points));
-        if (summary_csv) *summary_csv = dup(dsd::host::sweep_summary_csv(b.points));
+        if (csv_thread.joinable()) csv_thread.join();
+        if (summary_csv) *summary_csv = dup(csv);
+        tm.lap("summary");
         if (totals) {
             totals[0] = t.points;
             totals[1] = t.replicas;
@@ -262,7 +273,8 @@ int dsd_plan_sweep(const char* sweep_yaml, const char* base_dir, int shard, int 
         if (n_shards < 1 || shard < 0 || shard >= n_shards) throw dsd::Error(DSD_ERR_CONFIG, "bad shard index");
         dsd::cfg::Node node = dsd::cfg::parse(sweep_yaml ? sweep_yaml : "");
         auto p = std::make_unique<dsd_sweep_plan>();
-        p->b = dsd::host::plan_sweep(node, base_dir ? base_dir : ".", shard, n_shards, nullptr);
+        dsd::host::Caches caches;  // profiles / traces / models shared by the sweep's points
+        p->b = dsd::host::plan_sweep(node, base_dir ? base_dir : ".", shard, n_shards, &caches);
         for (size_t k = 0; k < p->b.resolved.size(); ++k) {
             p->b.resolved[k].bind();
             p->b.scenarios[k] = p->b.resolved[k].scen;

@@ -517,7 +517,7 @@ std::shared_ptr<const T> cached(Caches* caches, std::map<std::string, std::share
 }  // namespace
 
 Resolved resolve_config(const Node& config, bool strict, std::optional<uint64_t> seed_override,
-                        const std::string& base_dir, Caches* caches) {
+                        const std::string& base_dir, Caches* caches, bool want_digest) {
     Resolved rc;
     Topology topo = auto_topology(config, strict);
     // profile_from (runner.cpp:40-69)
@@ -550,7 +550,7 @@ Resolved resolve_config(const Node& config, bool strict, std::optional<uint64_t>
     }
     const uint64_t cfg_seed = static_cast<uint64_t>(config.int_or("seed", 42));
     rc.seed = seed_override.value_or(cfg_seed);
-    rc.digest = cfg::hex16(cfg::fnv1a64(config.canonical()));
+    if (want_digest) rc.digest = cfg::hex16(cfg::fnv1a64(config.canonical()));
     const Policy& pol = topo.policy;
     if (pol.window == DSD_WINDOW_AWC && !topo.drafts.empty()) {
         if (pol.model_path.empty()) config_error("window policy 'awc' requires policies.window.model");

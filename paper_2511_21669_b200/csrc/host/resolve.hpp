@@ -63,9 +63,10 @@ struct Resolved {
     void bind();  // (re)points scen's arrays at the owned vectors
 };
 
-// Throws dsd::Error.  `caches` may be null.
+// Throws dsd::Error.  `caches` may be null.  `want_digest` = false leaves
+// Resolved::digest empty (sweeps compute it only for report files).
 Resolved resolve_config(const cfg::Node& config, bool strict, std::optional<uint64_t> seed_override,
-                        const std::string& base_dir, Caches* caches);
+                        const std::string& base_dir, Caches* caches, bool want_digest = true);
 
 std::shared_ptr<const TraceData> load_trace_file(const std::string& path);
 std::shared_ptr<const TraceData> parse_trace_text(const std::string& text);

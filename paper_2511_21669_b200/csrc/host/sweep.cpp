@@ -6,8 +6,11 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <filesystem>
 #include <fstream>
+#include <cstdlib>
 #include <thread>
 
 #include "report.hpp"
@@ -53,6 +56,17 @@ uint64_t sweep_point_seed(uint64_t base_seed, const std::string& point_id, int r
     return cfg::fnv1a64(point_id + "#rep=" + std::to_string(repetition), base_seed ^ 0x9e3779b97f4a7c15ULL);
 }
 
+// sweep_point_seed for every repetition of one point: FNV-1a is a left fold,
+// so the point id is hashed once and each repetition continues from there.
+static void point_seeds(uint64_t base_seed, const std::string& point_id, int reps, std::vector<uint64_t>& out) {
+    out.resize(static_cast<size_t>(reps));
+    const uint64_t h = cfg::fnv1a64(point_id, base_seed ^ 0x9e3779b97f4a7c15ULL);
+    for (int r = 0; r < reps; ++r)
+        out[static_cast<size_t>(r)] = (r == 0 && point_id == "base")
+                                          ? base_seed
+                                          : cfg::fnv1a64("#rep=" + std::to_string(r), h);
+}
+
 namespace {
 
 std::string point_id_of(const std::vector<std::pair<std::string, std::string>>& assignment) {
@@ -76,44 +90,54 @@ std::string sanitize_filename(const std::string& s) {
 
 }  // namespace
 
+// The base config with point idx's axis values set (sweep.cpp:95-108).
+static Node point_config(const SweepSpec& spec, size_t idx) {
+    Node config = spec.base;
+    size_t rem = idx;
+    for (size_t a = spec.axes.size(); a-- > 0;) {
+        const auto& values = spec.axes[a].second;
+        cfg::set_path(config, spec.axes[a].first, values[rem % values.size()]);
+        rem /= values.size();
+    }
+    return config;
+}
+
+std::string point_digest(const SweepSpec& spec, size_t idx) {
+    return cfg::hex16(cfg::fnv1a64(point_config(spec, idx).canonical()));
+}
+
 SweepBatch plan_sweep(const Node& node, const std::string& base_dir, int shard, int n_shards, Caches* caches) {
     SweepBatch b;
     b.spec = SweepSpec::from_node(node, base_dir);
     const SweepSpec& spec = b.spec;
     const size_t n_points = spec.point_count();
     b.points.resize(n_points);
-    for (size_t idx = 0; idx < n_points; ++idx) {
-        size_t rem = idx;
-        auto& asg = b.points[idx].assignment;
-        for (size_t a = spec.axes.size(); a-- > 0;) {
-            const auto& values = spec.axes[a].second;
-            const Node& v = values[rem % values.size()];
-            rem /= values.size();
-            asg.emplace_back(spec.axes[a].first, v.scalar() ? v.to_string() : v.canonical());
-        }
-        std::reverse(asg.begin(), asg.end());
-        b.points[idx].point_id = point_id_of(asg);
-    }
-    // resolve every point once (seed-independent except for the seeds
-    // themselves, which become per-replica parameters)
+    // every point is materialised and resolved once, in parallel: assignment
+    // and id, the config, its scenario (the digest is only computed when
+    // report files are written) and the seeds of its repetitions
     std::vector<Resolved> res(n_points);
     std::vector<char> ok(n_points, 0);
+    std::vector<std::vector<uint64_t>> seeds(n_points);
     std::atomic<size_t> next{0};
     auto worker = [&] {
         for (;;) {
             size_t idx = next.fetch_add(1);
             if (idx >= n_points) return;
             SweepPoint& p = b.points[idx];
+            size_t rem = idx;
+            auto& asg = p.assignment;
+            for (size_t a = spec.axes.size(); a-- > 0;) {
+                const auto& values = spec.axes[a].second;
+                const Node& v = values[rem % values.size()];
+                rem /= values.size();
+                asg.emplace_back(spec.axes[a].first, v.scalar() ? v.to_string() : v.canonical());
+            }
+            std::reverse(asg.begin(), asg.end());
+            p.point_id = point_id_of(asg);
+            point_seeds(spec.base_seed, p.point_id, spec.repetitions, seeds[idx]);
             try {
-                Node config = spec.base;
-                size_t rem = idx;
-                for (size_t a = spec.axes.size(); a-- > 0;) {
-                    const auto& values = spec.axes[a].second;
-                    cfg::set_path(config, spec.axes[a].first, values[rem % values.size()]);
-                    rem /= values.size();
-                }
-                res[idx] = resolve_config(config, true, sweep_point_seed(spec.base_seed, p.point_id, 0),
-                                          spec.base_dir, caches);
+                res[idx] = resolve_config(point_config(spec, idx), true, seeds[idx][0], spec.base_dir, caches,
+                                          /*want_digest=*/false);
                 ok[idx] = 1;
             } catch (const std::exception& e) {
                 p.failed = true;
@@ -122,6 +146,7 @@ SweepBatch plan_sweep(const Node& node, const std::string& base_dir, int shard, 
         }
     };
     unsigned nthreads = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32u));
+    if (const char* e = std::getenv("DSD_HOST_THREADS")) nthreads = std::max(1, std::atoi(e));
     if (n_points < 64) nthreads = 1;
     if (nthreads == 1) {
         worker();
@@ -131,6 +156,9 @@ SweepBatch plan_sweep(const Node& node, const std::string& base_dir, int shard, 
         for (auto& t : pool) t.join();
     }
     b.point_scenario.assign(n_points, -1);
+    size_t n_ok = 0;
+    for (size_t idx = 0; idx < n_points; ++idx) n_ok += ok[idx];
+    b.resolved.reserve(n_ok);
     for (size_t idx = 0; idx < n_points; ++idx) {
         if (!ok[idx]) continue;
         b.point_scenario[idx] = static_cast<int64_t>(b.resolved.size());
@@ -141,6 +169,10 @@ SweepBatch plan_sweep(const Node& node, const std::string& base_dir, int shard, 
         r.bind();
         b.scenarios.push_back(r.scen);
     }
+    const size_t n_rep = n_ok * static_cast<size_t>(spec.repetitions);
+    const size_t mine = n_shards > 1 ? (n_rep + static_cast<size_t>(n_shards) - 1) / n_shards : n_rep;
+    b.replicas.reserve(mine);
+    b.replica_origin.reserve(mine);
     int64_t g = 0;
     for (size_t idx = 0; idx < n_points; ++idx) {
         const int64_t s = b.point_scenario[idx];
@@ -150,7 +182,7 @@ SweepBatch plan_sweep(const Node& node, const std::string& base_dir, int shard, 
             if (n_shards > 1 && g % n_shards != shard) continue;
             dsd_replica x{};
             x.scenario = static_cast<uint32_t>(s);
-            x.seed = sweep_point_seed(spec.base_seed, b.points[idx].point_id, rep);
+            x.seed = seeds[idx][static_cast<size_t>(rep)];
             x.gen_seed = r.gen_seed_fixed ? r.gen_seed : x.seed;
             b.replicas.push_back(x);
             b.replica_origin.emplace_back(static_cast<int64_t>(idx), rep);
@@ -159,20 +191,35 @@ SweepBatch plan_sweep(const Node& node, const std::string& base_dir, int shard, 
     return b;
 }
 
+PhaseTimer::PhaseTimer(const char* what) : what_(what), on_(std::getenv("DSD_HOST_TIMING") != nullptr) {
+    if (on_) t_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+void PhaseTimer::lap(const char* phase) {
+    if (!on_) return;
+    const double t = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    std::fprintf(stderr, "[dsd %s] %-10s %8.2f ms\n", what_, phase, t - t_);
+    t_ = t;
+}
+
 SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir) {
     SweepTotals tot;
+    PhaseTimer tm("run_sweep");
     const bool reports = !out_dir.empty();
     if (reports) std::filesystem::create_directories(out_dir);
     const size_t n = b.replicas.size();
     std::vector<dsd_replica_summary> sums(n);
     if (n > 0) {
         rt.prepare(b.scenarios.data(), b.scenarios.size(), b.replicas.data(), n, reports);
+        tm.lap("prepare");
         rt.launch();
         rt.sync();
+        tm.lap("kernels");
         rt.summaries(sums.data(), n);
+        tm.lap("summaries");
     }
     const int R = b.spec.repetitions;
     std::vector<double> thr(b.points.size(), 0.0), ttft(b.points.size(), 0.0), tpot(b.points.size(), 0.0);
+    std::vector<std::string> digest(reports ? b.points.size() : 0);  // config digests, on first use
     for (size_t k = 0; k < n; ++k) {  // replicas are point-major, rep-minor: sums in rep order
         const auto [p, rep] = b.replica_origin[k];
         SweepPoint& pt = b.points[static_cast<size_t>(p)];
@@ -204,10 +251,13 @@ SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir) {
                 out_dir + "/" + sanitize_filename(pt.point_id) + "_rep" + std::to_string(rep) + ".json";
             std::ofstream f(file, std::ios::binary);
             if (!f) throw Error(DSD_ERR_RUNTIME, "cannot write file: " + file);
-            f << emit_report(out, r.scen.n_targets, r.digest, b.replicas[k].seed);
+            std::string& dg = digest[static_cast<size_t>(p)];
+            if (dg.empty()) dg = point_digest(b.spec, static_cast<size_t>(p));
+            f << emit_report(out, r.scen.n_targets, dg, b.replicas[k].seed);
             pt.report_files.push_back(file);
         }
     }
+    tm.lap(reports ? "reports" : "aggregate");
     for (size_t p = 0; p < b.points.size(); ++p) {
         SweepPoint& pt = b.points[p];
         tot.points += 1;

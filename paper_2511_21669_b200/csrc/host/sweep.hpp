@@ -33,6 +33,8 @@ struct SweepPoint {
 };
 
 uint64_t sweep_point_seed(uint64_t base_seed, const std::string& point_id, int repetition);
+// config digest of point idx (the reference's per-run config_digest)
+std::string point_digest(const SweepSpec& spec, size_t idx);
 
 // Points resolved into scenarios + replicas (optionally one shard of them).
 struct SweepBatch {
@@ -46,6 +48,18 @@ struct SweepBatch {
 };
 
 SweepBatch plan_sweep(const cfg::Node& node, const std::string& base_dir, int shard, int n_shards, Caches* caches);
+
+// DSD_HOST_TIMING=1: phase durations of the host sweep path to stderr
+class PhaseTimer {
+  public:
+    explicit PhaseTimer(const char* what);
+    void lap(const char* phase);
+
+  private:
+    const char* what_;
+    bool on_;
+    double t_ = 0.0;
+};
 
 struct SweepTotals {
     double points = 0, replicas = 0, failed = 0, events = 0;
