@@ -100,8 +100,40 @@ __host__ __device__ inline int64_t smem_warp_bytes(int64_t ns, int64_t heap_cap)
 #endif
 constexpr uint32_t kBarrierKinds = DSD_BARRIER_KINDS;
 
+#ifndef DSD_VOTE_MODE
+#define DSD_VOTE_MODE 0
+#endif
+// The warp runs the pending kind with the highest score: lane count, ties to
+// the higher kind number.
+__device__ __forceinline__ unsigned vote_score(unsigned count, uint32_t kind) {
+#if DSD_VOTE_MODE == 1
+    return (count << 4) | (15u - kind);  // ties to the lower kind (decoded by vote_kind)
+#elif DSD_VOTE_MODE == 2
+    return ((kind == kActDispatch ? 2u * count : count) << 4) | kind;
+#elif DSD_VOTE_MODE == 3
+    return ((kind == kActBegin ? 2u * count : count) << 4) | kind;
+#elif DSD_VOTE_MODE == 4
+    return ((kind == kActItem ? 2u * count : count) << 4) | kind;
+#elif DSD_VOTE_MODE == 5
+    return ((kind == kActDispatch ? count + (count >> 1) : count) << 4) | kind;
+#else
+    return (count << 4) | kind;
+#endif
+}
+
+__device__ __forceinline__ uint32_t vote_kind(unsigned best) {
+#if DSD_VOTE_MODE == 1
+    return 15u - (best & 15u);
+#else
+    return best & 15u;
+#endif
+}
+
+#ifndef DSD_MIN_BLOCKS
+#define DSD_MIN_BLOCKS 8
+#endif
 template <bool kSmem, bool kStats>
-__global__ void __launch_bounds__(kBlock, 8) k_simulate(Workspace W, const int32_t* list, const int32_t* count,
+__global__ void __launch_bounds__(kBlock, DSD_MIN_BLOCKS) k_simulate(Workspace W, const int32_t* list, const int32_t* count,
                                                      int32_t smem_heap_cap) {
     int64_t rep = 0;
     const bool live = replica_of(W, list, count, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x, rep);
@@ -147,26 +179,24 @@ __global__ void __launch_bounds__(kBlock, 8) k_simulate(Workspace W, const int32
     for (;;) {
         // the kind most lanes have pending (majority vote)
         const unsigned peers = __match_any_sync(0xffffffffu, kind);
-        const unsigned score = kind == kActNone ? 0u : ((static_cast<unsigned>(__popc(peers)) << 4) | kind);
+        const unsigned score = kind == kActNone ? 0u : vote_score(static_cast<unsigned>(__popc(peers)), kind);
         const unsigned best = __reduce_max_sync(0xffffffffu, score);
         if (best == 0u) break;
-        if (kind == (best & 15u)) {
-            if constexpr (kStats) {
-                const long long t0 = clock64();
-                e.step();
-                const long long t1 = clock64();
-                atomicAdd(&blk_stats[2 * kind], static_cast<unsigned long long>(t1 - t0));
-                atomicAdd(&blk_stats[2 * kind + 1], 1ull);
-                kind = e.next_kind();
-            } else {
-                // the selected lanes run their continuation chain up to the
-                // next pop or dispatch: two "barrier" kinds per event keep the
-                // warp's lanes in phase, the short handlers in between ride along
-                do {
+        if (kind == vote_kind(best)) {
+            // the selected lanes run their continuation chain up to the next
+            // barrier kind (kBarrierKinds)
+            do {
+                if constexpr (kStats) {
+                    const long long t0 = clock64();
                     e.step();
-                    kind = e.next_kind();
-                } while (!((kBarrierKinds >> kind) & 1u));
-            }
+                    const long long t1 = clock64();
+                    atomicAdd(&blk_stats[2 * kind], static_cast<unsigned long long>(t1 - t0));
+                    atomicAdd(&blk_stats[2 * kind + 1], 1ull);
+                } else {
+                    e.step();
+                }
+                kind = e.next_kind();
+            } while (!((kBarrierKinds >> kind) & 1u));
         }
         if constexpr (kStats) ++iters;
     }
