@@ -165,7 +165,8 @@ typedef struct dsd_replica {
 
 typedef struct dsd_run_opts {
     int32_t collect_records; /* keep per-request records + sequences for dsd_fetch_records */
-    int32_t reserved;
+    int32_t feature_probe;   /* EngineOptions::feature_probe (engine.hpp:34): per-replica AWC
+                                feature sums, read back with dsd_batch_probe */
 } dsd_run_opts;
 
 /* Per-replica result: RunResult scalars (engine.hpp:44-53), the SystemMetrics
@@ -314,6 +315,37 @@ int dsd_emit_report(const dsd_replica_summary* summary, const dsd_request_record
 
 /* The canonical sweep seed derivation (sweep.cpp:51-57), exposed for tests. */
 uint64_t dsd_sweep_point_seed(uint64_t base_seed, const char* point_id, int repetition);
+
+/* After a batch prepared with dsd_run_opts.feature_probe: DSD_PROBE_FIELDS
+ * doubles per replica - the sums of the AWC feature vector over the
+ * iterations of requests with a draft server (features.cpp:5-13), their
+ * count (RunResult::mean_features = sums / count, engine.cpp:660-664), the
+ * sum of chosen windows (fused counted as 1) and the number of decisions. */
+#define DSD_PROBE_FIELDS 8
+int dsd_batch_probe(dsd_handle* h, double* out, size_t n, char* err, size_t errlen);
+
+/* ---- AWC dataset generation and policy evaluation ----
+ * build_scenarios (dataset.cpp:50-87) of a DatasetGrid YAML document
+ * (DatasetGrid::from_node, dataset.cpp:33-48; NULL or "" = the defaults),
+ * serialized as serialize_scenarios' JSONL (dataset.cpp:89-108).  Host only. */
+int dsd_build_scenarios(const char* grid_yaml, char** scenarios_jsonl, char* err, size_t errlen);
+
+/* generate_dataset (dataset.cpp:258-290) over build_scenarios(grid): every
+ * scenario x 12 candidates (static gamma 2..12, fused) as one device batch
+ * with the feature probe.  weights = {w_tpot, w_ttft, w_throughput} or NULL
+ * for ObjectiveWeights{} (dataset.hpp:55-59).  Returns serialize_dataset's
+ * JSONL (train.cpp:16-33) and the scenarios JSONL, as `specsim gen-dataset`
+ * writes dataset.jsonl / scenarios.jsonl (specsim_main.cpp:97-112). */
+int dsd_generate_dataset(dsd_handle* h, const char* grid_yaml, const double* weights, char** dataset_jsonl,
+                         char** scenarios_jsonl, char* err, size_t errlen);
+
+/* eval_policy_on_scenarios (dataset.cpp:292-369) on the scenarios of a
+ * scenarios JSONL whose split matches ("all" = every scenario; none ->
+ * DSD_ERR_CONFIG as specsim_main.cpp:131-138): window_kind static / dynamic /
+ * awc / fused with gamma and (awc) the model path.  out[4] = mean
+ * throughput_rps, mean_ttft_ms, mean_tpot_ms, mean chosen gamma. */
+int dsd_eval_policy(dsd_handle* h, const char* scenarios_jsonl, const char* split, const char* window_kind,
+                    int gamma, const char* model_path, double* out, char* err, size_t errlen);
 
 void dsd_free(void* p);
 

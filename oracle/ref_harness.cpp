@@ -399,4 +399,46 @@ int ref_awc_predict(const char* model_path, const double* features, std::size_t 
     });
 }
 
+// build_scenarios + serialize_scenarios (dataset.cpp:50-108) of a
+// DatasetGrid YAML document (DatasetGrid::from_node; empty = defaults).
+int ref_build_scenarios(const char* grid_yaml, char** scenarios_jsonl, char* err, std::size_t errlen) {
+    return guarded(err, errlen, [&] {
+        DatasetGrid g;
+        if (grid_yaml && *grid_yaml) g = DatasetGrid::from_node(yaml::parse_string(grid_yaml));
+        *scenarios_jsonl = dup_string(serialize_scenarios(build_scenarios(g)));
+    });
+}
+
+// `specsim gen-dataset` (specsim_main.cpp:97-112): generate_dataset over
+// build_scenarios(grid) with ObjectiveWeights{}, serialize_dataset.
+int ref_generate_dataset(const char* grid_yaml, int parallel, char** dataset_jsonl, char** scenarios_jsonl,
+                         char* err, std::size_t errlen) {
+    return guarded(err, errlen, [&] {
+        DatasetGrid g;
+        if (grid_yaml && *grid_yaml) g = DatasetGrid::from_node(yaml::parse_string(grid_yaml));
+        auto scenarios = build_scenarios(g);
+        auto samples = generate_dataset(scenarios, ObjectiveWeights{}, parallel);
+        *dataset_jsonl = dup_string(serialize_dataset(samples));
+        *scenarios_jsonl = dup_string(serialize_scenarios(scenarios));
+    });
+}
+
+// eval_policy_on_scenarios (dataset.cpp:292-369) on the scenarios of a
+// scenarios JSONL with the given split ("all" = every scenario).
+int ref_eval_policy(const char* scenarios_jsonl, const char* split, const char* window_kind, int gamma,
+                    const char* model_path, int parallel, double* out, char* err, std::size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::vector<ScenarioSpec> selected;
+        const std::string sp = split ? split : "all";
+        for (const auto& sc : parse_scenarios(scenarios_jsonl))
+            if (sp == "all" || sc.split == sp) selected.push_back(sc);
+        if (selected.empty()) throw ConfigError("no scenarios with split '" + sp + "'");
+        PolicyEval e = eval_policy_on_scenarios(selected, window_kind, gamma, model_path ? model_path : "", parallel);
+        out[0] = e.mean_throughput_rps;
+        out[1] = e.mean_ttft_ms;
+        out[2] = e.mean_tpot_ms;
+        out[3] = e.mean_chosen_gamma;
+    });
+}
+
 }  // extern "C"

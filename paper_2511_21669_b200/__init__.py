@@ -5,7 +5,7 @@ layer + sm_100a CUDA kernels.  This package is the thin Python mirror used by
 tests and bench.py; see DESIGN.md.
 """
 from .api import (ConfigError, DsdError, EngineError, SimulationOutput, Simulator, SweepOutput, SUMMARY_DTYPE,
-                  run_simulation, run_sweep, sweep_point_seed)
+                  build_scenarios, run_simulation, run_sweep, sweep_point_seed)
 
 __all__ = ["ConfigError", "DsdError", "EngineError", "SimulationOutput", "Simulator", "SweepOutput",
-           "SUMMARY_DTYPE", "run_simulation", "run_sweep", "sweep_point_seed"]
+           "SUMMARY_DTYPE", "build_scenarios", "run_simulation", "run_sweep", "sweep_point_seed"]

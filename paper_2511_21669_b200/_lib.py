@@ -60,8 +60,10 @@ EXPORTS = [
     "dsd_run_simulation", "dsd_run_sweep", "dsd_prepare_sweep", "dsd_resolve_config", "dsd_resolved_scenario",
     "dsd_resolved_replica", "dsd_resolved_digest", "dsd_resolved_free", "dsd_plan_sweep",
     "dsd_sweep_plan_scenarios", "dsd_sweep_plan_replicas", "dsd_sweep_plan_origin", "dsd_sweep_plan_free", "dsd_emit_report",
-    "dsd_sweep_point_seed", "dsd_free",
+    "dsd_sweep_point_seed", "dsd_free", "dsd_batch_probe", "dsd_build_scenarios", "dsd_generate_dataset",
+    "dsd_eval_policy",
 ]
+DSD_PROBE_FIELDS = 8
 
 _lib = None
 
@@ -126,5 +128,9 @@ def lib():
                                   c.POINTER(c.c_int64), c.c_int, cp, c.c_uint64, c.POINTER(vp), c.POINTER(vp)]
     L.dsd_sweep_point_seed.argtypes = [c.c_uint64, cp, c.c_int]
     L.dsd_sweep_point_seed.restype = c.c_uint64
+    L.dsd_batch_probe.argtypes = [vp, c.POINTER(c.c_double), sz, cp, sz]
+    L.dsd_build_scenarios.argtypes = [cp, c.POINTER(vp), cp, sz]
+    L.dsd_generate_dataset.argtypes = [vp, cp, c.POINTER(c.c_double), c.POINTER(vp), c.POINTER(vp), cp, sz]
+    L.dsd_eval_policy.argtypes = [vp, cp, cp, cp, c.c_int, cp, c.POINTER(c.c_double), cp, sz]
     _lib = L
     return L

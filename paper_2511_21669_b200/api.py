@@ -206,6 +206,39 @@ class Simulator:
         self._L.dsd_last_kernel_ms(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(t))
         return {"sim_ms": a.value, "stage_ms": b.value, "total_ms": t.value}
 
+    # ---- AWC dataset generation / policy evaluation (dataset.cpp) ----
+    def generate_dataset(self, grid: str = "", weights=None):
+        """`specsim gen-dataset`: (dataset.jsonl text, scenarios.jsonl text) for a
+        DatasetGrid YAML document or file ("" = DatasetGrid defaults); weights =
+        (w_tpot, w_ttft, w_throughput) or None for ObjectiveWeights{}."""
+        text, _ = _text(grid) if grid else ("", None)
+        c = ctypes
+        ds, sc = c.c_void_p(), c.c_void_p()
+        w = (c.c_double * 3)(*weights) if weights is not None else None
+        err = c.create_string_buffer(4096)
+        _check(self._L.dsd_generate_dataset(self._h, text.encode(), w, c.byref(ds), c.byref(sc), err, 4096), err)
+        return _take(ds), _take(sc)
+
+    def eval_policy(self, scenarios_jsonl: str, window_kind: str, gamma: int = 4, model_path: str = "",
+                    split: str = "all") -> dict:
+        """eval_policy_on_scenarios over the scenarios of `split`."""
+        c = ctypes
+        out = (c.c_double * 4)()
+        err = c.create_string_buffer(4096)
+        _check(self._L.dsd_eval_policy(self._h, scenarios_jsonl.encode(), split.encode(), window_kind.encode(), gamma,
+                                       model_path.encode(), out, err, 4096), err)
+        return {"policy": window_kind, "throughput_rps": out[0], "mean_ttft_ms": out[1], "mean_tpot_ms": out[2],
+                "mean_gamma": out[3]}
+
+    def probe(self, n: Optional[int] = None) -> np.ndarray:
+        """[n, DSD_PROBE_FIELDS] feature-probe sums of the last probed batch."""
+        n = self.n_replicas if n is None else n
+        out = np.zeros((n, _lib.DSD_PROBE_FIELDS), dtype=np.float64)
+        err = ctypes.create_string_buffer(1024)
+        _check(self._L.dsd_batch_probe(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n, err, 1024),
+               err)
+        return out
+
 
 _default: Optional[Simulator] = None
 
@@ -228,3 +261,13 @@ def run_sweep(spec: str, base_dir: Optional[str] = None, out_dir: str = "") -> S
 
 def sweep_point_seed(base_seed: int, point_id: str, repetition: int) -> int:
     return int(_lib.lib().dsd_sweep_point_seed(base_seed, point_id.encode(), repetition))
+
+
+def build_scenarios(grid: str = "") -> str:
+    """build_scenarios + serialize_scenarios (host only): scenarios.jsonl text
+    for a DatasetGrid YAML document or file ("" = the defaults)."""
+    text, _ = _text(grid) if grid else ("", None)
+    p = ctypes.c_void_p()
+    err = ctypes.create_string_buffer(4096)
+    _check(_lib.lib().dsd_build_scenarios(text.encode(), ctypes.byref(p), err, 4096), err)
+    return _take(p)

@@ -153,6 +153,76 @@ DSD_HD_NOINLINE double awc_predict(const char* blob, const DevScenario& S, const
 }
 
 // ---------------------------------------------------------------------------
+// pair / target metric rings (MetricsCollector, metrics.cpp:40-128) and the
+// AWC feature vector, as free functions over the workspace: the feature code
+// runs out of line (AWC decisions and the feature probe only), which keeps it
+// out of the event loop's instruction footprint
+// ---------------------------------------------------------------------------
+// warp-interleaved per-replica arrays in HBM (pair stats, busy export)
+template <typename U>
+DSD_HD U& il_at(U* base, int32_t rep, int64_t cap, int64_t idx) {
+    return base[((static_cast<int64_t>(rep) >> 5) * cap + idx) * kLanes + (rep & 31)];
+}
+
+// acceptance_recent (metrics.cpp:93-108): ring sums in storage order
+DSD_HD double acceptance_recent_at(const Workspace& W, int32_t rep, int64_t p) {
+    int32_t cnt = il_at(W.p_acc_cnt, rep, W.c.np, p);
+    int64_t ex = 0, ac = 0;
+    for (int k = 0; k < cnt; ++k) {
+        ex += il_at(W.p_acc_ex, rep, W.c.np * 20, p * 20 + k);
+        ac += il_at(W.p_acc_ac, rep, W.c.np * 20, p * 20 + k);
+    }
+    if (ex == 0) return 0.5;
+    return static_cast<double>(ac) / static_cast<double>(ex);
+}
+
+// extract_features (features.cpp:5-13) for pair p = (d, t): queue pressure
+// (open requests of the target / queue capacity, clamped), recent
+// acceptance, recent RTT (the link's nominal RTT before any sample), recent
+// TPOT of the target, the pair's previous window
+DSD_HD_NOINLINE void extract_features(const Workspace& W, int32_t rep, int64_t p, int32_t t, int32_t open_t,
+                                      int32_t queue_capacity, double link_rtt_ms, double* f) {
+    double q = static_cast<double>(open_t) / static_cast<double>(queue_capacity);
+    f[0] = q < 0.0 ? 0.0 : (q > 1.0 ? 1.0 : q);
+    f[1] = acceptance_recent_at(W, rep, p);
+    int32_t rc = il_at(W.p_rtt_cnt, rep, W.c.np, p);
+    if (rc == 0) {
+        f[2] = link_rtt_ms;
+    } else {
+        double sum = 0.0;
+        for (int k = 0; k < rc; ++k) sum += il_at(W.p_rtt, rep, W.c.np * 20, p * 20 + k);
+        f[2] = sum / static_cast<double>(rc);
+    }
+    int32_t tc = il_at(W.t_tcnt, rep, W.c.nt, t);
+    if (tc == 0) {
+        f[3] = 0.0;
+    } else {
+        double sum = 0.0;
+        for (int k = 0; k < tc; ++k) sum += il_at(W.t_tpot, rep, W.c.nt * 50, static_cast<int64_t>(t) * 50 + k);
+        f[3] = sum / static_cast<double>(tc);
+    }
+    f[4] = static_cast<double>(il_at(W.p_gprev, rep, W.c.np, p));
+}
+
+// EngineOptions::feature_probe (engine.cpp:376-381, 660-664) plus the
+// chosen-window tally eval_policy_on_scenarios reads from the records
+// (dataset.cpp:344-351, fused counts as 1): per-replica sums in
+// W.probe[rep][kProbeFields], accumulated in event order.  p < 0: the
+// request has no draft server (no feature sample).
+DSD_HD_NOINLINE void probe_iteration(const Workspace& W, int32_t rep, int64_t p, int32_t t, int32_t open_t,
+                                     int32_t queue_capacity, double link_rtt_ms, int32_t chosen) {
+    double* pr = W.probe + static_cast<int64_t>(rep) * kProbeFields;
+    if (p >= 0) {
+        double f[5];
+        extract_features(W, rep, p, t, open_t, queue_capacity, link_rtt_ms, f);
+        for (int k = 0; k < 5; ++k) pr[k] += f[k];
+        pr[5] += 1.0;
+    }
+    pr[6] += static_cast<double>(chosen);
+    pr[7] += 1.0;
+}
+
+// ---------------------------------------------------------------------------
 // the engine
 //
 // Control flow is continuation-passing: the reference's nested call chains
@@ -341,13 +411,6 @@ struct Engine {
     DSD_HD ReqRec& slot(int32_t d) const {
         return *reinterpret_cast<ReqRec*>(hotb + static_cast<int64_t>(d) * kLanes * kHotStride);
     }
-    // the first kHotBitWords acceptance-bit words of draft d's active session,
-    // lane-interleaved after the session slots (word k at [k * kLanes])
-    DSD_HD uint64_t* hot_bits(int32_t d) const {
-        const int lane = rep & 31;
-        unsigned char* base = hotb - lane * kHotStride + static_cast<int64_t>(nsc - 1) * kLanes * kHotStride;
-        return reinterpret_cast<uint64_t*>(base) + lane + d * kHotBitWords * kLanes;
-    }
     DSD_HD ReqRec& rec(int64_t i) const {
         if (hotb) {
             for (int32_t d = 0; d < D; ++d)
@@ -441,16 +504,6 @@ struct Engine {
 
     // ---- metrics hooks (metrics.cpp:40-128) ----
     DSD_HD int64_t pair_of(int32_t d, int32_t t) const { return static_cast<int64_t>(d) * T + t; }
-    DSD_HD double acceptance_recent(int64_t p) const {
-        int32_t cnt = IL(W.p_acc_cnt, W.c.np, p);
-        int64_t ex = 0, ac = 0;
-        for (int k = 0; k < cnt; ++k) {
-            ex += IL(W.p_acc_ex, W.c.np * 20, p * 20 + k);
-            ac += IL(W.p_acc_ac, W.c.np * 20, p * 20 + k);
-        }
-        if (ex == 0) return 0.5;
-        return static_cast<double>(ac) / static_cast<double>(ex);
-    }
     // fixed-capacity ring insert: returns the storage slot (metrics.cpp:55-72)
     static DSD_HD int64_t ring_slot(int32_t& cnt, int32_t& pos, int cap) {
         if (cnt < cap) return cnt++;
@@ -482,6 +535,7 @@ struct Engine {
         bool fused;
         int gamma;
     };
+
     DSD_HD Decision decide_window(int64_t i) {
         const ReqRec& r = rec(i);
         int32_t d = D > 0 ? r.drafter : -1;
@@ -492,7 +546,7 @@ struct Engine {
                 return Decision{false, gamma_s};
             case 1: {  // window_dynamic (policies.cpp:60-68)
                 int64_t p = pair_of(d, t);
-                double a = acceptance_recent(p);
+                double a = acceptance_recent_at(W, rep, p);
                 int32_t& g = IL(W.p_dyn, W.c.np, p);
                 if (a > 0.75 && g < S.gamma_max) {
                     ++g;
@@ -504,27 +558,7 @@ struct Engine {
             case 2: {  // AWC: extract_features -> predict_gamma -> stabilized_decide
                 int64_t p = pair_of(d, t);
                 double f[5];
-                // features.cpp:5-13
-                double q = static_cast<double>(SV(v_open, t)) / static_cast<double>(S.queue_capacity);
-                f[0] = q < 0.0 ? 0.0 : (q > 1.0 ? 1.0 : q);
-                f[1] = acceptance_recent(p);
-                int32_t rc = IL(W.p_rtt_cnt, W.c.np, p);
-                if (rc == 0) {
-                    f[2] = link(d, t).rtt_ms;
-                } else {
-                    double sum = 0.0;
-                    for (int k = 0; k < rc; ++k) sum += IL(W.p_rtt, W.c.np * 20, p * 20 + k);
-                    f[2] = sum / static_cast<double>(rc);
-                }
-                int32_t tc = IL(W.t_tcnt, W.c.nt, t);
-                if (tc == 0) {
-                    f[3] = 0.0;
-                } else {
-                    double sum = 0.0;
-                    for (int k = 0; k < tc; ++k) sum += IL(W.t_tpot, W.c.nt * 50, static_cast<int64_t>(t) * 50 + k);
-                    f[3] = sum / static_cast<double>(tc);
-                }
-                f[4] = static_cast<double>(IL(W.p_gprev, W.c.np, p));
+                extract_features(W, rep, p, t, SV(v_open, t), S.queue_capacity, link(d, t).rtt_ms, f);
                 double raw = awc_predict(W.blob, S, f);
                 // stabilized_decide (smoother.cpp:8-37)
                 const double gmin = static_cast<double>(S.gamma_min);
@@ -796,6 +830,9 @@ struct Engine {
         if (phase(r) == kPhDone) return;
         int32_t d = D > 0 ? r.drafter : -1;
         int32_t t = r.target;
+        if (W.probe)  // before the pair's previous window is overwritten
+            probe_iteration(W, rep, d >= 0 ? pair_of(d, t) : -1, t, SV(v_open, t), S.queue_capacity,
+                            d >= 0 ? link(d, t).rtt_ms : 0.0, dec.fused ? 1 : dec.gamma);
         if (d >= 0 && t >= 0 && ps()) IL(W.p_gprev, W.c.np, pair_of(d, t)) = dec.fused ? 1 : dec.gamma;
         if (dec.fused) {
             set_flag(r, kFused, true);
@@ -925,6 +962,8 @@ struct Engine {
             st[4] = 0;
         }
         jitter.seed(seed, kLabelJitter);
+        if (W.probe)
+            for (int k = 0; k < kProbeFields; ++k) W.probe[static_cast<int64_t>(rep) * kProbeFields + k] = 0.0;
         N = (S.workload == 0) ? S.n_requests : S.tr_n;
         seq_next = static_cast<uint32_t>(N);
         if (N > 0) next_arr_t = R[arrival_index(0)].arrival;

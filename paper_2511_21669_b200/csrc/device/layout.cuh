@@ -24,7 +24,7 @@ constexpr int kServerFields = 8;
 // sessions live in shared memory; a replica whose dynamic event heap outgrows
 // it is re-run on the HBM variant.
 constexpr int kSmemServers = 4;
-constexpr int kHotBitWords = 4;  // acceptance-bit words of an active session kept in shared memory
+constexpr int kProbeFields = 8;  // Workspace::probe entries per replica
 
 // Event kinds (proj/include/specsim/sim/event_queue.hpp:12-18).
 enum : uint32_t { kEvArrival = 0, kEvBatchReady = 1, kEvComputeDone = 2, kEvNetArrive = 3, kEvIterStart = 4 };
@@ -193,6 +193,9 @@ struct Workspace {
     uint64_t* h_key;     // seq<<32 | info
     // ---- acceptance bits: replica-contiguous [n][bw] ----
     uint64_t* bits;
+    // ---- optional feature probe (dsd_run_opts.feature_probe): [n][kProbeFields]
+    // feature sums f0..f4, feature samples, chosen-window sum, decisions
+    double* probe;
     // ---- optional step profile (DSD_STEP_STATS=1): [2k] cycles, [2k+1] count
     // per step kind, [32] warp iterations, [33] warp cycles, [34] max iterations
     unsigned long long* step_stats;

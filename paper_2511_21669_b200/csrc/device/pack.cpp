@@ -71,7 +71,7 @@ int64_t axis_table(BlobBuilder& B, const double* axis, int n, int32_t* size) {
 
 }  // namespace
 
-Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n) {
+Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n, bool probe) {
     if (ns == 0 && n > 0) cfg_error("batch has replicas but no scenarios");
     Packed P;
     BlobBuilder B;
@@ -210,8 +210,9 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
         d.gamma_min = s.gamma_min;
         d.gamma_max = s.gamma_max;
         d.queue_capacity = s.queue_capacity;
-        d.pair_stats = (!d.fused_everything && (s.window_kind == DSD_WINDOW_DYNAMIC ||
-                                                 s.window_kind == DSD_WINDOW_AWC))
+        d.pair_stats = ((!d.fused_everything && (s.window_kind == DSD_WINDOW_DYNAMIC ||
+                                                  s.window_kind == DSD_WINDOW_AWC)) ||
+                        (probe && s.n_drafts > 0))
                            ? 1
                            : 0;
         if (s.window_kind == DSD_WINDOW_AWC && !d.fused_everything) {

@@ -18,8 +18,11 @@ struct Packed {
 };
 
 // Validates the scenarios (reference error texts, DSD_ERR_CONFIG) and packs
-// them into the scenario blob; computes the batch capacities.
-Packed pack_batch(const dsd_scenario* scenarios, size_t n_scenarios, const dsd_replica* replicas, size_t n);
+// them into the scenario blob; computes the batch capacities.  `probe`: the
+// batch runs with the feature probe, so every scenario with draft servers
+// keeps the pair metric rings (the reference always does).
+Packed pack_batch(const dsd_scenario* scenarios, size_t n_scenarios, const dsd_replica* replicas, size_t n,
+                  bool probe = false);
 
 // Assigns the workspace field pointers inside [base, base + bytes) and
 // returns bytes; with base == nullptr it only sizes.

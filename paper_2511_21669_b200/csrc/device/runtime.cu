@@ -133,7 +133,8 @@ __device__ __forceinline__ uint32_t vote_kind(unsigned best) {
 #define DSD_MIN_BLOCKS 8
 #endif
 template <bool kSmem, bool kStats>
-__global__ void __launch_bounds__(kBlock, DSD_MIN_BLOCKS) k_simulate(Workspace W, const int32_t* list, const int32_t* count,
+__global__ void __launch_bounds__(kBlock, DSD_MIN_BLOCKS) k_simulate(const __grid_constant__ Workspace W,
+                                                                      const int32_t* list, const int32_t* count,
                                                      int32_t smem_heap_cap) {
     int64_t rep = 0;
     const bool live = replica_of(W, list, count, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x, rep);
@@ -268,7 +269,7 @@ struct RuntimeImpl {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[4] = {};
-    DevBuf blob, scen, reps, arena, summary, fail, ltot, seqbase, seqg, seqc, rec, busy, ovf;
+    DevBuf blob, scen, reps, arena, summary, fail, ltot, seqbase, seqg, seqc, rec, busy, ovf, probe;
     // shared-memory heap slots per replica for small topologies (0 = always
     // run the HBM variant; env DSD_SMEM_HEAP overrides, for tests)
     // 7: with 8 server fields x 2 servers and one session slot a warp needs
@@ -334,13 +335,13 @@ void Runtime::transfer_bytes(int64_t* h2d, int64_t* d2h) const {
 }
 
 void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n,
-                      bool collect) {
+                      bool collect, bool feature_probe) {
     RuntimeImpl& R = *impl_;
     DSD_CUDA(cudaSetDevice(R.device));
     R.prepared = false;
     R.ran = false;
     R.rec_cached = false;
-    Packed P = pack_batch(sc, ns, reps, n);
+    Packed P = pack_batch(sc, ns, reps, n, feature_probe);
     const Caps& c = P.caps;
     // ---- upload blob, scenarios, replicas ----
     R.blob.ensure(P.blob.size());
@@ -382,6 +383,10 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
     W.summary = static_cast<DevSummary*>(R.summary.p);
     W.fail = static_cast<int32_t*>(R.fail.p);
     W.collect = collect ? 1 : 0;
+    if (feature_probe) {
+        R.probe.ensure(sizeof(double) * kProbeFields * std::max<size_t>(n, 1));
+        W.probe = static_cast<double*>(R.probe.p);
+    }
     R.host_scen = std::move(P.scen);
     R.n = n;
     R.collect = collect;
@@ -499,6 +504,17 @@ void Runtime::summaries(dsd_replica_summary* out, size_t n) {
     if (n) DSD_CUDA(cudaMemcpyAsync(out, R.summary.p, sizeof(DevSummary) * n, cudaMemcpyDeviceToHost, R.stream));
     R.d2h_bytes += static_cast<int64_t>(sizeof(DevSummary) * n);
     DSD_CUDA(cudaStreamSynchronize(R.stream));
+}
+
+static_assert(kProbeFields == DSD_PROBE_FIELDS, "probe layout must match include/dsdsim.h");
+
+void Runtime::probe(double* out, size_t n) {
+    RuntimeImpl& R = *impl_;
+    if (!R.ran || !R.W.probe) throw Error(DSD_ERR_RUNTIME, "the batch did not run with the feature probe");
+    if (n > R.n) n = R.n;
+    DSD_CUDA(cudaSetDevice(R.device));
+    DSD_CUDA(cudaStreamSynchronize(R.stream));
+    if (n) DSD_CUDA(cudaMemcpy(out, R.W.probe, sizeof(double) * kProbeFields * n, cudaMemcpyDeviceToHost));
 }
 
 void Runtime::device_summaries(void** ptr, size_t* bytes) {

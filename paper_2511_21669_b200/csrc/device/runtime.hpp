@@ -29,8 +29,9 @@ public:
     Runtime& operator=(const Runtime&) = delete;
 
     // Packs + uploads scenarios and replicas and sizes the workspace.
+    // feature_probe: accumulate the per-replica probe sums (probe()).
     void prepare(const dsd_scenario* scenarios, size_t n_scenarios, const dsd_replica* replicas,
-                 size_t n, bool collect_records);
+                 size_t n, bool collect_records, bool feature_probe = false);
     // Enqueues the staging + simulation kernels on the handle's stream.
     void launch();
     void sync();
@@ -39,6 +40,8 @@ public:
                        int32_t* gamma_seq, int32_t* committed_seq, size_t seq_cap, int64_t* n_seq,
                        int64_t* busy_us, size_t busy_cap);
     void device_summaries(void** ptr, size_t* bytes);
+    // After a probed run: [n][kProbeFields] sums per replica (see Workspace::probe).
+    void probe(double* out, size_t n);
     void* stream();
     int64_t last_launch_count() const;
     void last_kernel_ms(double* sim_ms, double* gen_ms, double* total_ms);

@@ -11,6 +11,7 @@
 #include "dsdsim.h"
 #include "report.hpp"
 #include "resolve.hpp"
+#include "dataset.hpp"
 #include "sweep.hpp"
 
 struct dsd_handle {
@@ -77,7 +78,7 @@ int dsd_run_batch(dsd_handle* h, const dsd_scenario* scenarios, size_t n_scenari
                   size_t n, const dsd_run_opts* opts, dsd_replica_summary* summaries, char* err, size_t errlen) {
     return guard(err, errlen, [&] {
         need(h);
-        h->rt->prepare(scenarios, n_scenarios, replicas, n, opts && opts->collect_records);
+        h->rt->prepare(scenarios, n_scenarios, replicas, n, opts && opts->collect_records, opts && opts->feature_probe);
         h->rt->launch();
         h->rt->sync();
         if (summaries && n) h->rt->summaries(summaries, n);
@@ -98,7 +99,7 @@ int dsd_batch_prepare(dsd_handle* h, const dsd_scenario* scenarios, size_t n_sce
                       size_t n, const dsd_run_opts* opts, char* err, size_t errlen) {
     return guard(err, errlen, [&] {
         need(h);
-        h->rt->prepare(scenarios, n_scenarios, replicas, n, opts && opts->collect_records);
+        h->rt->prepare(scenarios, n_scenarios, replicas, n, opts && opts->collect_records, opts && opts->feature_probe);
     });
 }
 
@@ -324,6 +325,61 @@ int dsd_emit_report(const dsd_replica_summary* summary, const dsd_request_record
 
 uint64_t dsd_sweep_point_seed(uint64_t base_seed, const char* point_id, int repetition) {
     return dsd::host::sweep_point_seed(base_seed, point_id ? point_id : "", repetition);
+}
+
+
+int dsd_batch_probe(dsd_handle* h, double* out, size_t n, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        if (!out && n) throw dsd::Error(DSD_ERR_RUNTIME, "null output buffer");
+        h->rt->probe(out, n);
+    });
+}
+
+int dsd_build_scenarios(const char* grid_yaml, char** scenarios_jsonl, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        dsd::cfg::Node node = dsd::cfg::parse(grid_yaml ? grid_yaml : "");
+        auto sc = dsd::host::build_scenarios(dsd::host::DatasetGrid::from_node(node));
+        if (scenarios_jsonl) *scenarios_jsonl = dup(dsd::host::serialize_scenarios(sc));
+    });
+}
+
+int dsd_generate_dataset(dsd_handle* h, const char* grid_yaml, const double* weights, char** dataset_jsonl,
+                         char** scenarios_jsonl, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        dsd::cfg::Node node = dsd::cfg::parse(grid_yaml ? grid_yaml : "");
+        auto sc = dsd::host::build_scenarios(dsd::host::DatasetGrid::from_node(node));
+        dsd::host::ObjectiveWeights w;
+        if (weights) {
+            w.w_tpot = weights[0];
+            w.w_ttft = weights[1];
+            w.w_throughput = weights[2];
+        }
+        auto sweeps = dsd::host::generate_dataset(*h->rt, sc, w, &h->caches);
+        if (dataset_jsonl) *dataset_jsonl = dup(dsd::host::serialize_dataset(sweeps));
+        if (scenarios_jsonl) *scenarios_jsonl = dup(dsd::host::serialize_scenarios(sc));
+    });
+}
+
+int dsd_eval_policy(dsd_handle* h, const char* scenarios_jsonl, const char* split, const char* window_kind,
+                    int gamma, const char* model_path, double* out, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        const std::string sp = split ? split : "all";
+        std::vector<dsd::host::ScenarioSpec> selected;
+        for (const auto& s : dsd::host::parse_scenarios(scenarios_jsonl ? scenarios_jsonl : ""))
+            if (sp == "all" || s.split == sp) selected.push_back(s);
+        if (selected.empty()) throw dsd::Error(DSD_ERR_CONFIG, "no scenarios with split '" + sp + "'");
+        auto e = dsd::host::eval_policy_on_scenarios(*h->rt, selected, window_kind ? window_kind : "static", gamma,
+                                                      model_path ? model_path : "", &h->caches);
+        if (out) {
+            out[0] = e.mean_throughput_rps;
+            out[1] = e.mean_ttft_ms;
+            out[2] = e.mean_tpot_ms;
+            out[3] = e.mean_chosen_gamma;
+        }
+    });
 }
 
 }  // extern "C"

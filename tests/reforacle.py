@@ -56,6 +56,11 @@ def lib():
                                              c.POINTER(c.c_int)]
         L.ref_predict_synth.restype = c.c_double
         L.ref_predict_synth.argtypes = [c.c_double] * 5 + [c.c_int, c.c_int, c.c_int, c.c_int, c.c_int64]
+        L.ref_build_scenarios.argtypes = [c.c_char_p, c.POINTER(c.c_void_p), c.c_char_p, c.c_size_t]
+        L.ref_generate_dataset.argtypes = [c.c_char_p, c.c_int, c.POINTER(c.c_void_p), c.POINTER(c.c_void_p),
+                                           c.c_char_p, c.c_size_t]
+        L.ref_eval_policy.argtypes = [c.c_char_p, c.c_char_p, c.c_char_p, c.c_int, c.c_char_p, c.c_int,
+                                      c.POINTER(c.c_double), c.c_char_p, c.c_size_t]
         _lib = L
     return _lib
 
@@ -160,6 +165,40 @@ def train_model(path, parallel=8, epochs=0, seed=42):
     if rc != 0:
         raise RefError(rc, err.value.decode())
     return list(maes)
+
+
+def build_scenarios(grid_yaml=""):
+    """build_scenarios + serialize_scenarios of the reference (dataset.cpp:50-108)."""
+    c = ctypes
+    p = c.c_void_p()
+    err = c.create_string_buffer(4096)
+    rc = lib().ref_build_scenarios(grid_yaml.encode(), c.byref(p), err, 4096)
+    if rc != 0:
+        raise RefError(rc, err.value.decode())
+    return _take(p)
+
+
+def generate_dataset(grid_yaml="", parallel=8):
+    """`specsim gen-dataset`: (dataset.jsonl, scenarios.jsonl) text of the reference."""
+    c = ctypes
+    ds, sc = c.c_void_p(), c.c_void_p()
+    err = c.create_string_buffer(4096)
+    rc = lib().ref_generate_dataset(grid_yaml.encode(), parallel, c.byref(ds), c.byref(sc), err, 4096)
+    if rc != 0:
+        raise RefError(rc, err.value.decode())
+    return _take(ds), _take(sc)
+
+
+def eval_policy(scenarios_jsonl, window_kind, gamma=4, model_path="", split="all", parallel=8):
+    """eval_policy_on_scenarios of the reference -> [thr, ttft, tpot, mean gamma]."""
+    c = ctypes
+    out = (c.c_double * 4)()
+    err = c.create_string_buffer(4096)
+    rc = lib().ref_eval_policy(scenarios_jsonl.encode(), split.encode(), window_kind.encode(), gamma,
+                               model_path.encode(), parallel, out, err, 4096)
+    if rc != 0:
+        raise RefError(rc, err.value.decode())
+    return list(out)
 
 
 def sha256(s):
