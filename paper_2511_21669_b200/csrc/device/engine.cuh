@@ -885,6 +885,24 @@ struct Engine {
         const uint64_t* bits = W.bits + static_cast<int64_t>(rep) * W.c.bw + r.bitoff;
         const int32_t nb = r.nbits;
         int32_t cur = r.cursor;
+        if (gamma > 0 && gamma <= 64 && cur + gamma <= nb) {
+            // no wrap inside the window: the accepted prefix is the run of
+            // trailing ones of the gamma bits at the cursor
+            const int s = cur & 63;
+            uint64_t w = bits[cur >> 6] >> s;
+            if (s + gamma > 64) w |= bits[(cur >> 6) + 1] << (64 - s);
+            const uint64_t zeros = ~w;
+#ifdef __CUDA_ARCH__
+            const int ones = zeros ? __ffsll(static_cast<long long>(zeros)) - 1 : 64;
+#else
+            const int ones = zeros ? __builtin_ctzll(zeros) : 64;
+#endif
+            accepted = ones < gamma ? ones : gamma;
+            consumed = accepted < gamma ? accepted + 1 : gamma;
+            cur += consumed;
+            r.cursor = cur == nb ? 0 : cur;
+            return;
+        }
         accepted = 0;
         consumed = 0;
         while (consumed < gamma) {

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -341,7 +342,18 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
     R.prepared = false;
     R.ran = false;
     R.rec_cached = false;
+    // DSD_HOST_TIMING=1: phase durations to stderr
+    static const bool timing = std::getenv("DSD_HOST_TIMING") != nullptr;
+    auto t_prev = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!timing) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[dsd prepare] %-10s %8.2f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t - t_prev).count());
+        t_prev = t;
+    };
     Packed P = pack_batch(sc, ns, reps, n, feature_probe);
+    lap("pack");
     const Caps& c = P.caps;
     // ---- upload blob, scenarios, replicas ----
     R.blob.ensure(P.blob.size());
@@ -367,6 +379,7 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
     // ---- workspace arena ----
     Workspace& W = R.W;
     W = Workspace{};
+    lap("upload");
     const size_t total = layout_workspace(W, c, nullptr);
     size_t free_b = 0, total_b = 0;
     DSD_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -391,7 +404,9 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
     R.n = n;
     R.collect = collect;
     if (collect) R.ltot.ensure(sizeof(int64_t) * std::max<size_t>(n, 1));
+    lap("workspace");
     DSD_CUDA(cudaStreamSynchronize(R.stream));
+    lap("sync");
     R.prepared = true;
 }
 
