@@ -301,15 +301,33 @@ struct Engine {
     // has_order<<8 | single_link<<9 | batching_window<<10
     uint32_t pflags;
     int32_t gamma_s, max_batch, dmax_batch;
+    // Specialised instantiation for batches whose every scenario is a single
+    // (target, draft) pair with a static window, FIFO batching, no batching
+    // window, a jitter-free link, no pair statistics, no probe and no record
+    // collection (Runtime::launch checks; the C5 sweep is one).  The kernel
+    // passes a compile-time true, so T, D and the policy flags below become
+    // constants and the generic paths fold away: a smaller, faster event loop.
+    bool spec;
+    static constexpr uint32_t kSpecFlags = (1u << 3) | (1u << 9);  // jitter_free | single_link
 
     DSD_HD Engine(const Workspace& w, const DevScenario& s, int64_t replica, int32_t* server_base,
                   int64_t* heap_time_base, uint64_t* heap_key_base, int64_t heap_cap, int32_t server_cap,
-                  unsigned char* hot_base = nullptr)
+                  unsigned char* hot_base = nullptr, bool specialized = false)
         : W(w), S(s), rep(static_cast<int32_t>(replica)), sb(server_base), htb(heap_time_base),
-          hkb(heap_key_base), hcap(static_cast<int32_t>(heap_cap)), nsc(server_cap) {
+          hkb(heap_key_base), hcap(static_cast<int32_t>(heap_cap)), nsc(server_cap), spec(specialized) {
+        R = W.req + replica * W.c.nr;
+        gamma_s = S.gamma;
+        max_batch = S.max_batch;
+        dmax_batch = S.draft_max_batch;
+        if (spec) {
+            T = 1;
+            D = 1;
+            hotb = hot_base;
+            pflags = kSpecFlags;
+            return;
+        }
         T = S.n_targets;
         D = S.n_drafts;
-        R = W.req + replica * W.c.nr;
         hotb = S.fused_everything ? nullptr : hot_base;
         pflags = static_cast<uint32_t>(S.fused_everything) | (static_cast<uint32_t>(S.pair_stats) << 1) |
                  (static_cast<uint32_t>(S.batching == 1) << 2) | (static_cast<uint32_t>(S.jitter_free) << 3) |
@@ -317,10 +335,10 @@ struct Engine {
                  (static_cast<uint32_t>(S.has_order != 0) << 8) |
                  (static_cast<uint32_t>(S.n_dg == 1 && S.n_tg == 1) << 9) |
                  (static_cast<uint32_t>(S.batching_window_us > 0) << 10);
-        gamma_s = S.gamma;
-        max_batch = S.max_batch;
-        dmax_batch = S.draft_max_batch;
     }
+    DSD_HD bool hot() const { return spec || hotb != nullptr; }
+    DSD_HD bool collecting() const { return !spec && W.collect; }
+    DSD_HD bool probing() const { return !spec && W.probe != nullptr; }
     DSD_HD bool fe() const { return pflags & 1u; }
     DSD_HD bool ps() const { return (pflags >> 1) & 1u; }
     DSD_HD bool lab_batching() const { return (pflags >> 2) & 1u; }
@@ -412,7 +430,7 @@ struct Engine {
         return *reinterpret_cast<ReqRec*>(hotb + static_cast<int64_t>(d) * kLanes * kHotStride);
     }
     DSD_HD ReqRec& rec(int64_t i) const {
-        if (hotb) {
+        if (hot()) {
             for (int32_t d = 0; d < D; ++d)
                 if (SV(v_active, T + d) == static_cast<int32_t>(i)) return slot(d);
         }
@@ -738,7 +756,7 @@ struct Engine {
     // ---- request lifecycle ----
     DSD_HD void record_gamma(ReqRec& r, int g) {
         int32_t n = r.ng;
-        if (W.collect) {
+        if (collecting()) {
             int64_t o = W.rep_seqbase[rep] + r.seqoff + n;
             if (o < W.seq_cap) W.seq_gamma[o] = g; else fail = kFailSeq;
         }
@@ -746,7 +764,7 @@ struct Engine {
     }
     DSD_HD void record_commit(ReqRec& r, int c) {
         int32_t n = r.nc;
-        if (W.collect) {
+        if (collecting()) {
             int64_t o = W.rep_seqbase[rep] + r.seqoff + n;
             if (o < W.seq_cap) W.seq_commit[o] = c; else fail = kFailSeq;
         }
@@ -762,7 +780,7 @@ struct Engine {
         int32_t nx = g.snext;
         SV(v_shead, v) = nx;
         if (nx < 0) SV(v_stail, v) = -1;
-        if (hotb) copy_rec(slot(d), g);
+        if (hot()) copy_rec(slot(d), g);
         SV(v_active, v) = i;
         enqueue(v, i, 1, kOpPrefill, g.prompt, false);
     }
@@ -830,7 +848,7 @@ struct Engine {
         if (phase(r) == kPhDone) return;
         int32_t d = D > 0 ? r.drafter : -1;
         int32_t t = r.target;
-        if (W.probe)  // before the pair's previous window is overwritten
+        if (probing())  // before the pair's previous window is overwritten
             probe_iteration(W, rep, d >= 0 ? pair_of(d, t) : -1, t, SV(v_open, t), S.queue_capacity,
                             d >= 0 ? link(d, t).rtt_ms : 0.0, dec.fused ? 1 : dec.gamma);
         if (d >= 0 && t >= 0 && ps()) IL(W.p_gprev, W.c.np, pair_of(d, t)) = dec.fused ? 1 : dec.gamma;
@@ -863,7 +881,7 @@ struct Engine {
         if (d >= 0) {
             int32_t v = T + d;
             if (SV(v_active, v) == static_cast<int32_t>(i)) {
-                if (hotb) copy_rec(R[i], slot(d));  // write the session back
+                if (hot()) copy_rec(R[i], slot(d));  // write the session back
                 SV(v_active, v) = -1;
                 push_act(act(kActActivate, static_cast<uint32_t>(d)));
             }
@@ -980,7 +998,7 @@ struct Engine {
             st[4] = 0;
         }
         jitter.seed(seed, kLabelJitter);
-        if (W.probe)
+        if (probing())
             for (int k = 0; k < kProbeFields; ++k) W.probe[static_cast<int64_t>(rep) * kProbeFields + k] = 0.0;
         N = (S.workload == 0) ? S.n_requests : S.tr_n;
         seq_next = static_cast<uint32_t>(N);
@@ -1145,7 +1163,7 @@ struct Engine {
     // Engine::finish (engine.cpp:648-669) + aggregate_run (runner.cpp:153-169)
     DSD_HD void finish() {
         for (int32_t v = 0; v < T; ++v) IL(W.v_busy_us, W.c.ns, v) = get_busy(v);  // for the records export
-        if (hotb)  // sessions still active (a failed replica stops early): write them back
+        if (hot())  // sessions still active (a failed replica stops early): write them back
             for (int32_t d = 0; d < D; ++d) {
                 const int32_t a = SV(v_active, T + d);
                 if (a >= 0) copy_rec(R[a], slot(d));

@@ -133,7 +133,8 @@ __device__ __forceinline__ uint32_t vote_kind(unsigned best) {
 #ifndef DSD_MIN_BLOCKS
 #define DSD_MIN_BLOCKS 8
 #endif
-template <bool kSmem, bool kStats>
+// kSpec: the single-pair specialisation (Engine::spec; kSmem only).
+template <bool kSmem, bool kStats, bool kSpec = false>
 __global__ void __launch_bounds__(kBlock, DSD_MIN_BLOCKS) k_simulate(const __grid_constant__ Workspace W,
                                                                       const int32_t* list, const int32_t* count,
                                                      int32_t smem_heap_cap) {
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(kBlock, DSD_MIN_BLOCKS) k_simulate(const __gri
     if constexpr (kSmem) {
         extern __shared__ __align__(16) unsigned char smem[];
         const int lane = threadIdx.x % kLanes;
-        nsc = static_cast<int32_t>(W.c.ns);
+        nsc = kSpec ? 2 : static_cast<int32_t>(W.c.ns);
         hcap = smem_heap_cap;
         const int64_t srv_bytes = static_cast<int64_t>(kServerFields) * nsc * kLanes * 4;
         unsigned char* blk = smem + (threadIdx.x / kLanes) * smem_warp_bytes(nsc, hcap);
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(kBlock, DSD_MIN_BLOCKS) k_simulate(const __gri
         hb = W.h_time + w * W.c.hc * kLanes + lane;
         kb = W.h_key + w * W.c.hc * kLanes + lane;
     }
-    Engine e(W, W.scen[W.rep_scen[r]], r, sbase, hb, kb, hcap, nsc, hot);
+    Engine e(W, W.scen[W.rep_scen[r]], r, sbase, hb, kb, hcap, nsc, hot, kSpec);
     if (live) e.init();
     uint32_t kind = live ? e.next_kind() : static_cast<uint32_t>(kActNone);
     // kStats: per-step-kind cycle profile (DSD_STEP_STATS=1), one block-level
@@ -277,6 +278,10 @@ struct RuntimeImpl {
     // 9.75 KB, so 8 blocks/SM fit the 164 KB carveout (L1 keeps 92 KB)
     int32_t smem_heap = 7;
     bool step_stats = false;  // env DSD_STEP_STATS=1: per-step-kind cycle profile to stderr
+    // every scenario of the prepared batch fits the single-pair kernel
+    // specialisation (Engine::spec); env DSD_SPECIALIZE=0 disables its use
+    bool spec_ok = false;
+    bool specialize = true;
     DevBuf stats;
     Workspace W{};
     std::vector<DevScenario> host_scen;
@@ -310,9 +315,11 @@ Runtime::Runtime(int device) : impl_(new RuntimeImpl) {
     DSD_CUDA(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking));
     if (const char* h = std::getenv("DSD_SMEM_HEAP")) impl_->smem_heap = std::max(0, std::atoi(h));
     if (const char* s = std::getenv("DSD_STEP_STATS")) impl_->step_stats = std::atoi(s) != 0;
+    if (const char* s = std::getenv("DSD_SPECIALIZE")) impl_->specialize = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_CARVEOUT")) {  // shared-memory share of the L1/smem array (%)
         const int pct = std::atoi(s);
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     }
     for (auto& ev : impl_->ev) DSD_CUDA(cudaEventCreate(&ev));
@@ -400,6 +407,11 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
         R.probe.ensure(sizeof(double) * kProbeFields * std::max<size_t>(n, 1));
         W.probe = static_cast<double*>(R.probe.p);
     }
+    R.spec_ok = c.ns == 2;
+    for (const DevScenario& d : P.scen)
+        R.spec_ok = R.spec_ok && d.n_targets == 1 && d.n_drafts == 1 && !d.fused_everything && d.window_kind == 0 &&
+                    d.batching == 0 && d.batching_window_us == 0 && d.jitter_free && d.n_dg == 1 && d.n_tg == 1 &&
+                    !d.has_order && !d.pair_stats;
     R.host_scen = std::move(P.scen);
     R.n = n;
     R.collect = collect;
@@ -455,7 +467,13 @@ void Runtime::launch() {
     const bool smem = R.W.c.ns <= kSmemServers && R.smem_heap > 0;
     if (smem) {
         const size_t bytes = static_cast<size_t>(kBlock / kLanes) * smem_warp_bytes(R.W.c.ns, R.smem_heap);
-        (R.step_stats ? k_simulate<true, true> : k_simulate<true, false>)<<<grid, kBlock, bytes, R.stream>>>(R.W, nullptr, nullptr, R.smem_heap);
+        const bool spec = R.spec_ok && R.specialize && !R.collect && !R.W.probe;
+        if (spec)
+            (R.step_stats ? k_simulate<true, true, true> : k_simulate<true, false, true>)<<<grid, kBlock, bytes, R.stream>>>(
+                R.W, nullptr, nullptr, R.smem_heap);
+        else
+            (R.step_stats ? k_simulate<true, true> : k_simulate<true, false>)<<<grid, kBlock, bytes, R.stream>>>(
+                R.W, nullptr, nullptr, R.smem_heap);
         DSD_CUDA(cudaGetLastError());
         // replicas whose event heap outgrew shared memory run again from HBM
         R.ovf.ensure(4 * (R.n + 1));

@@ -116,3 +116,33 @@ def test_kernel_variants_and_overflow_rerun(smem_heap):
     finally:
         del os.environ["DSD_SMEM_HEAP"]
     assert out.summary_json == js
+
+
+@pytest.mark.parametrize("smem_heap", ["7", "2"])
+def test_specialized_kernel_matches_generic_and_reference(smem_heap):
+    """A sweep whose every point is a single (target, draft) pair with a static
+    window runs the specialised kernel (Engine::spec): its per-replica
+    summaries must equal the generic kernel's bit for bit (DSD_SPECIALIZE=0),
+    and its sweep summary the reference's; heap 2 forces overflow re-runs."""
+    from paper_2511_21669_b200 import Simulator
+    spec = ("base: c1_single_pair.yaml\nseed: 5\nrepetitions: 3\naxes:\n"
+            "  policies.window.gamma: [1, 4, 9, 16]\n  network.rtt_ms: [2, 30]\n"
+            "  workload.acceptance_rate: [0.5, 0.9]\n  workload.rate_rps: [2, 40]\n")
+    js, _ = ref.run_sweep(spec, CFG, 4)
+    sums = {}
+    for specialize in ("1", "0"):
+        os.environ["DSD_SPECIALIZE"] = specialize
+        os.environ["DSD_SMEM_HEAP"] = smem_heap
+        try:
+            with Simulator(0) as s:
+                s.prepare_sweep(spec, base_dir=CFG)
+                s.launch()
+                s.sync()
+                sums[specialize] = s.summaries()
+                assert s.run_sweep(spec, base_dir=CFG).summary_json == js
+        finally:
+            del os.environ["DSD_SPECIALIZE"]
+            del os.environ["DSD_SMEM_HEAP"]
+    assert len(sums["1"]) == 32 * 3
+    assert (sums["1"]["status"] == 0).all()
+    assert sums["1"].tobytes() == sums["0"].tobytes()
