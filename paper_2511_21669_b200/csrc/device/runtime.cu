@@ -282,6 +282,10 @@ struct RuntimeImpl {
     // specialisation (Engine::spec); env DSD_SPECIALIZE=0 disables its use
     bool spec_ok = false;
     bool specialize = true;
+    // shared-memory carveout of the kSmem kernels (% of the SM's maximum):
+    // -1 = sized per launch (Runtime::launch), env DSD_CARVEOUT fixes it
+    int carveout = -1;
+    int sms = 148, smem_per_sm = 228 * 1024;
     DevBuf stats;
     Workspace W{};
     std::vector<DevScenario> host_scen;
@@ -317,11 +321,12 @@ Runtime::Runtime(int device) : impl_(new RuntimeImpl) {
     if (const char* s = std::getenv("DSD_STEP_STATS")) impl_->step_stats = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_SPECIALIZE")) impl_->specialize = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_CARVEOUT")) {  // shared-memory share of the L1/smem array (%)
-        const int pct = std::atoi(s);
-        DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-        DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-        DSD_CUDA(cudaFuncSetAttribute(k_simulate<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        impl_->carveout = std::atoi(s);
+        DSD_CUDA(cudaFuncSetAttribute(k_simulate<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      impl_->carveout));
     }
+    DSD_CUDA(cudaDeviceGetAttribute(&impl_->sms, cudaDevAttrMultiProcessorCount, device));
+    DSD_CUDA(cudaDeviceGetAttribute(&impl_->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
     for (auto& ev : impl_->ev) DSD_CUDA(cudaEventCreate(&ev));
 }
 
@@ -467,6 +472,20 @@ void Runtime::launch() {
     const bool smem = R.W.c.ns <= kSmemServers && R.smem_heap > 0;
     if (smem) {
         const size_t bytes = static_cast<size_t>(kBlock / kLanes) * smem_warp_bytes(R.W.c.ns, R.smem_heap);
+        // Carveout: just the shared memory of the blocks one wave puts on an
+        // SM (1 KB of it reserved per block); the rest of the 256 KB array is
+        // L1.  The driver's default sizes for the launch-bounds maximum (8
+        // blocks) even when 65,536 replicas need 7 per SM, costing 32-64 KB of L1.
+        int pct = R.carveout;
+        if (pct < 0) {
+            const int64_t per_sm = std::min<int64_t>(DSD_MIN_BLOCKS, (grid + R.sms - 1) / R.sms);
+            const int64_t need = per_sm * (static_cast<int64_t>(bytes) + 1024);
+            pct = static_cast<int>(std::min<int64_t>(100, (100 * need + R.smem_per_sm - 1) / R.smem_per_sm));
+        }
+        DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         const bool spec = R.spec_ok && R.specialize && !R.collect && !R.W.probe;
         if (spec)
             (R.step_stats ? k_simulate<true, true, true> : k_simulate<true, false, true>)<<<grid, kBlock, bytes, R.stream>>>(
