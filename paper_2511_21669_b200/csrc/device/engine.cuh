@@ -436,12 +436,28 @@ struct Engine {
         }
         return R[i];
     }
-    // out of line: runs twice per request (activation, write-back)
-    static DSD_HD_NOINLINE void copy_rec(ReqRec& dst, const ReqRec& src) {
+    static DSD_HD void copy_rec_inline(ReqRec& dst, const ReqRec& src) {
         uint64_t* d = reinterpret_cast<uint64_t*>(&dst);
         const uint64_t* s = reinterpret_cast<const uint64_t*>(&src);
+        uint64_t v[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) d[k] = s[k];
+        for (int k = 0; k < 16; ++k) v[k] = s[k];  // all loads first: one memory latency
+#pragma unroll
+        for (int k = 0; k < 16; ++k) d[k] = v[k];
+    }
+    // out of line in the generic kernel (its code size is the constraint);
+    // runs twice per request (activation, write-back)
+    static DSD_HD_NOINLINE void copy_rec_call(ReqRec& dst, const ReqRec& src) { copy_rec_inline(dst, src); }
+    DSD_HD void copy_rec(ReqRec& dst, const ReqRec& src) const {
+        if (spec) copy_rec_inline(dst, src); else copy_rec_call(dst, src);
+    }
+    // pulls a queued session's record towards L2 ahead of its activation
+    DSD_HD void prefetch_l2(int32_t i) const {
+#ifdef __CUDA_ARCH__
+        if (i >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(R + i));
+#else
+        (void)i;
+#endif
     }
 
     // ---- event heap: SimKernel::schedule (event_queue.cpp:20-26) ----
@@ -780,7 +796,10 @@ struct Engine {
         int32_t nx = g.snext;
         SV(v_shead, v) = nx;
         if (nx < 0) SV(v_stail, v) = -1;
-        if (hot()) copy_rec(slot(d), g);
+        if (hot()) {
+            copy_rec(slot(d), g);
+            prefetch_l2(nx);  // the next session's copy-in is one activation away
+        }
         SV(v_active, v) = i;
         enqueue(v, i, 1, kOpPrefill, g.prompt, false);
     }
@@ -1090,19 +1109,16 @@ struct Engine {
         }
     }
 
-    // Executes exactly one step of kind next_kind().
-    DSD_HD void step() {
-        if (sp == 0) {
-            pop_event();
-            return;
-        }
-        const uint32_t a = pop_act();
-        const uint32_t arg = a >> 4;
-        switch (a & 15u) {
-            case kActDispatch: try_dispatch(static_cast<int32_t>(arg >> 1), arg & 1u); break;
+    static DSD_HD uint32_t opaque(uint32_t x) {
+#ifdef __CUDA_ARCH__
+        asm volatile("" : "+r"(x));
+#endif
+        return x;
+    }
+    // the once-per-request steps
+    DSD_HD void step_rare(uint32_t k, uint32_t arg) {
+        switch (k) {
             case kActActivate: activate_next_session(static_cast<int32_t>(arg)); break;
-            case kActItem: item_done(static_cast<int32_t>(arg)); break;
-            case kActBegin: begin(arg >> 1, arg & 1u); break;
             case kActFinish: finish_request(arg); break;
             case kActSendPrompt: {
                 const ReqRec& r = rec(arg);
@@ -1111,40 +1127,59 @@ struct Engine {
                 break;
             }
             case kActArrival: on_arrival(arg); break;
-            case kActNetPrompt: {  // on_net_arrive (engine.cpp:406-435)
+            default: {  // kActNetPrompt: on_net_arrive (engine.cpp:406-435)
                 const ReqRec& r = rec(arg);
                 enqueue(r.target, arg, 0, kOpPrefill, r.prompt, true);
                 break;
             }
-            case kActNetProposal: {
-                ReqRec& r = rec(arg);
-                set_phase(r, kPhVerifying);
-                enqueue(r.target, arg, 1, kOpVerify, r.pgamma, true);
-                break;
+        }
+    }
+
+    // Executes exactly one step of kind next_kind().
+    DSD_HD void step() {
+        if (sp == 0) {
+            pop_event();
+            return;
+        }
+        const uint32_t a = pop_act();
+        const uint32_t arg = a >> 4;
+        const uint32_t k = a & 15u;
+        // the frequent kinds as a branch chain in C5 frequency order (dispatch,
+        // batch item, compute done, iteration start, proposal, result), the
+        // rare ones through a switch: no indirect jump on the hot path (each
+        // test reads the kind through opaque() so the compiler cannot fold
+        // the chain back into a jump table)
+        if (opaque(k) == kActDispatch) {
+            try_dispatch(static_cast<int32_t>(arg >> 1), arg & 1u);
+        } else if (opaque(k) == kActItem) {
+            item_done(static_cast<int32_t>(arg));
+        } else if (opaque(k) == kActComputeDone) {  // on_compute_done (engine.cpp:569-589)
+            const int32_t v = static_cast<int32_t>(arg);
+            set_busy_flag(v, false);
+            const int32_t head = SV(v_run, v);
+            SV(v_run, v) = -1;
+            push_act(act(kActDispatch, static_cast<uint32_t>(v) * 2));
+            if (head >= 0) {
+                item_server = v;
+                push_act(act(kActItem, static_cast<uint32_t>(head)));
             }
-            case kActNetResult: {  // on_result_at_draft (engine.cpp:428-435)
-                ReqRec& r = rec(arg);
-                if (ps())
-                    on_rtt_sample(r.drafter, r.target, static_cast<double>(static_cast<int64_t>(r.outd) + r.backd) / 1000.0);
-                if (commit_tokens(r, r.lcr)) {
-                    push_act(act(kActFinish, arg));
-                } else {
-                    defer(now, info(kEvIterStart, 0, arg));
-                }
-                break;
+        } else if (opaque(k) == kActBegin) {
+            begin(arg >> 1, arg & 1u);
+        } else if (opaque(k) == kActNetProposal) {
+            ReqRec& r = rec(arg);
+            set_phase(r, kPhVerifying);
+            enqueue(r.target, arg, 1, kOpVerify, r.pgamma, true);
+        } else if (opaque(k) == kActNetResult) {  // on_result_at_draft (engine.cpp:428-435)
+            ReqRec& r = rec(arg);
+            if (ps())
+                on_rtt_sample(r.drafter, r.target, static_cast<double>(static_cast<int64_t>(r.outd) + r.backd) / 1000.0);
+            if (commit_tokens(r, r.lcr)) {
+                push_act(act(kActFinish, arg));
+            } else {
+                defer(now, info(kEvIterStart, 0, arg));
             }
-            default: {  // kActComputeDone: on_compute_done (engine.cpp:569-589)
-                const int32_t v = static_cast<int32_t>(arg);
-                set_busy_flag(v, false);
-                const int32_t head = SV(v_run, v);
-                SV(v_run, v) = -1;
-                push_act(act(kActDispatch, static_cast<uint32_t>(v) * 2));
-                if (head >= 0) {
-                    item_server = v;
-                    push_act(act(kActItem, static_cast<uint32_t>(head)));
-                }
-                break;
-            }
+        } else {
+            step_rare(k, arg);
         }
         if (pend_t >= 0) {
             schedule(pend_t, pend_info);
