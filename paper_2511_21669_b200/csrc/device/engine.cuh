@@ -309,6 +309,10 @@ struct Engine {
     // constants and the generic paths fold away: a smaller, faster event loop.
     bool spec;
     static constexpr uint32_t kSpecFlags = (1u << 3) | (1u << 9);  // jitter_free | single_link
+    // specialised kernel only: the four latency grids (target / draft x
+    // prefill / decode-shaped) and the link's one-way delay, resolved once
+    const DevGrid *g_tp = nullptr, *g_td = nullptr, *g_dp = nullptr, *g_dd = nullptr;
+    int64_t link_us = 0;
 
     DSD_HD Engine(const Workspace& w, const DevScenario& s, int64_t replica, int32_t* server_base,
                   int64_t* heap_time_base, uint64_t* heap_key_base, int64_t heap_cap, int32_t server_cap,
@@ -324,6 +328,14 @@ struct Engine {
             D = 1;
             hotb = hot_base;
             pflags = kSpecFlags;
+            const int32_t* tg = blob_ptr<int32_t>(W.blob, S.o_tgrid);
+            const int32_t* dg = blob_ptr<int32_t>(W.blob, S.o_dgrid);
+            const DevGrid* grids = blob_ptr<DevGrid>(W.blob, S.o_grids);
+            g_tp = grids + tg[0];
+            g_td = grids + tg[1];
+            g_dp = grids + dg[0];
+            g_dd = grids + dg[1];
+            link_us = blob_ptr<DevLink>(W.blob, S.o_links)[0].fixed_us;
             return;
         }
         T = S.n_targets;
@@ -527,6 +539,7 @@ struct Engine {
         return links[dg[d] * S.n_tg + tg[t]];
     }
     DSD_HD int64_t net_delay(int32_t d, int32_t t) {
+        if (spec) return link_us;  // one jitter-free link
         const DevLink& lk = link(d, t);
         if (jitter_free()) return lk.fixed_us;  // the jitter stream is unobservable
         double rtt = lk.rtt_ms, jit = lk.jitter_ms;
@@ -749,15 +762,20 @@ struct Engine {
         }
         if (taken == 0) return;  // nothing eligible (the reference's empty candidate list)
         // LatencyProfile::predict (profile.cpp:129-151) on the server's grids
-        const int32_t* gi = is_draft ? blob_ptr<int32_t>(W.blob, S.o_dgrid) + 2 * (v - T)
-                                     : blob_ptr<int32_t>(W.blob, S.o_tgrid) + 2 * v;
-        const DevGrid* grids = blob_ptr<DevGrid>(W.blob, S.o_grids);
         const bool prefill = kind == static_cast<int32_t>(kOpPrefill);
         const bool decode = kind == static_cast<int32_t>(kOpDecode);
         // queries: (batch, prompt tokens) / (batch, context) / (batch*tokens, context)
         const int64_t qb = (prefill || decode) ? taken : taken * tok;
         const int64_t qc = prefill ? static_cast<int64_t>(tok) : ctx;
-        const DevGrid& g = grids[gi[prefill ? 0 : 1]];
+        const DevGrid* gp;
+        if (spec) {
+            gp = is_draft ? (prefill ? g_dp : g_dd) : (prefill ? g_tp : g_td);
+        } else {
+            const int32_t* gi = is_draft ? blob_ptr<int32_t>(W.blob, S.o_dgrid) + 2 * (v - T)
+                                         : blob_ptr<int32_t>(W.blob, S.o_tgrid) + 2 * v;
+            gp = blob_ptr<DevGrid>(W.blob, S.o_grids) + gi[prefill ? 0 : 1];
+        }
+        const DevGrid& g = *gp;
         double ms = g.o_btab >= 0 && g.o_ctab >= 0
                         ? grid_interpolate_int(W.blob, g, qb, qc)
                         : grid_interpolate(W.blob, g, static_cast<double>(qb), static_cast<double>(qc));
