@@ -393,11 +393,13 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
     W = Workspace{};
     lap("upload");
     const size_t total = layout_workspace(W, c, nullptr);
-    size_t free_b = 0, total_b = 0;
-    DSD_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    if (total > R.arena.bytes && total + (256u << 20) > free_b + R.arena.bytes)
-        throw Error(DSD_ERR_RUNTIME, "replica workspace (" + std::to_string(total >> 20) +
-                                         " MiB) exceeds free device memory");
+    if (total > R.arena.bytes) {  // growing: check the device has room (cudaMemGetInfo is not free)
+        size_t free_b = 0, total_b = 0;
+        DSD_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        if (total + (256u << 20) > free_b + R.arena.bytes)
+            throw Error(DSD_ERR_RUNTIME, "replica workspace (" + std::to_string(total >> 20) +
+                                             " MiB) exceeds free device memory");
+    }
     R.arena.ensure(total);
     layout_workspace(W, c, static_cast<char*>(R.arena.p));
     W.blob = static_cast<const char*>(R.blob.p);

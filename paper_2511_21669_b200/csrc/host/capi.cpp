@@ -202,13 +202,15 @@ int dsd_run_sweep(dsd_handle* h, const char* sweep_yaml, const char* base_dir, c
         tm.lap("parse");
         dsd::host::SweepBatch b = dsd::host::plan_sweep(node, base_dir ? base_dir : ".", 0, 1, &h->caches);
         tm.lap("plan");
-        dsd::host::SweepTotals t = dsd::host::run_sweep(*h->rt, b, out_dir ? out_dir : "");
+        dsd::host::SummaryParts parts;
+        const bool text = summary_json || summary_csv;
+        dsd::host::SweepTotals t = dsd::host::run_sweep(*h->rt, b, out_dir ? out_dir : "", text ? &parts : nullptr);
         tm.lap("run");
         // the two summary texts are independent: build the CSV alongside the JSON
         std::string csv;
         std::thread csv_thread;
-        if (summary_csv) csv_thread = std::thread([&] { csv = dsd::host::sweep_summary_csv(b.points); });
-        if (summary_json) *summary_json = dup(dsd::host::sweep_summary_json(b.points));
+        if (summary_csv) csv_thread = std::thread([&] { csv = dsd::host::assemble_summary_csv(parts, b.points); });
+        if (summary_json) *summary_json = dup(dsd::host::assemble_summary_json(parts, b.points));
         if (csv_thread.joinable()) csv_thread.join();
         if (summary_csv) *summary_csv = dup(csv);
         tm.lap("summary");

@@ -201,7 +201,7 @@ void PhaseTimer::lap(const char* phase) {
     t_ = t;
 }
 
-SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir) {
+SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir, SummaryParts* parts) {
     SweepTotals tot;
     PhaseTimer tm("run_sweep");
     const bool reports = !out_dir.empty();
@@ -212,6 +212,9 @@ SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir) {
         rt.prepare(b.scenarios.data(), b.scenarios.size(), b.replicas.data(), n, reports);
         tm.lap("prepare");
         rt.launch();
+        // the host is idle while the kernels run: render the summary text
+        // that does not depend on the results
+        if (parts) *parts = render_summary_prefixes(b.points);
         rt.sync();
         tm.lap("kernels");
         rt.summaries(sums.data(), n);
@@ -220,6 +223,7 @@ SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir) {
     const int R = b.spec.repetitions;
     std::vector<double> thr(b.points.size(), 0.0), ttft(b.points.size(), 0.0), tpot(b.points.size(), 0.0);
     std::vector<std::string> digest(reports ? b.points.size() : 0);  // config digests, on first use
+    if (n == 0 && parts) *parts = render_summary_prefixes(b.points);
     for (size_t k = 0; k < n; ++k) {  // replicas are point-major, rep-minor: sums in rep order
         const auto [p, rep] = b.replica_origin[k];
         SweepPoint& pt = b.points[static_cast<size_t>(p)];
@@ -272,41 +276,79 @@ SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir) {
     return tot;
 }
 
-std::string sweep_summary_json(const std::vector<SweepPoint>& points) {
-    JsonOut w;
-    w.open_object();
-    w.key("points").open_array();
-    for (const auto& p : points) {
-        w.open_object();
-        w.key("point").str(p.point_id);
-        w.key("assignment").open_object();
-        for (const auto& kv : p.assignment) w.key(kv.first).str(kv.second);
-        w.close_object();
-        w.key("failed").boolean(p.failed);
-        if (p.failed) {
-            w.key("error").str(p.error);
-        } else {
-            w.key("throughput_rps").fixed(p.mean_throughput_rps, 6);
-            w.key("mean_ttft_ms").fixed(p.mean_ttft_ms, 3);
-            w.key("mean_tpot_ms").fixed(p.mean_tpot_ms, 3);
+// sweep_summary_json / sweep_summary_csv (sweep.cpp:164-199) in the layout
+// JsonOut writes (2-space indent), split per point into the part that is
+// known before the simulation (id, assignment) and the part that needs its
+// results, so run_sweep renders the former while the kernels run.
+SummaryParts render_summary_prefixes(const std::vector<SweepPoint>& points) {
+    SummaryParts parts;
+    parts.json.resize(points.size());
+    parts.csv.resize(points.size());
+    for (size_t i = 0; i < points.size(); ++i) {
+        const SweepPoint& p = points[i];
+        std::string& j = parts.json[i];
+        j += i ? ",\n    {\n      \"point\": \"" : "\n    {\n      \"point\": \"";
+        cfg::json_escape(j, p.point_id);
+        j += "\",\n      \"assignment\": {";
+        for (size_t k = 0; k < p.assignment.size(); ++k) {
+            j += k ? ",\n        \"" : "\n        \"";
+            cfg::json_escape(j, p.assignment[k].first);
+            j += "\": \"";
+            cfg::json_escape(j, p.assignment[k].second);
+            j += '"';
         }
-        w.close_object();
+        j += p.assignment.empty() ? "}" : "\n      }";
+        j += ",\n      \"failed\": ";
+        parts.csv[i] = "\"" + p.point_id + "\",";
     }
-    w.close_array();
-    w.close_object();
-    std::string out = w.take();
-    out += '\n';
+    return parts;
+}
+
+std::string assemble_summary_json(const SummaryParts& parts, const std::vector<SweepPoint>& points) {
+    std::string out = "{\n  \"points\": [";
+    for (size_t i = 0; i < points.size(); ++i) {
+        const SweepPoint& p = points[i];
+        out += parts.json[i];
+        if (p.failed) {
+            out += "true,\n      \"error\": \"";
+            cfg::json_escape(out, p.error);
+            out += "\"\n    }";
+        } else {
+            out += "false,\n      \"throughput_rps\": ";
+            out += cfg::fmt_fixed(p.mean_throughput_rps, 6);
+            out += ",\n      \"mean_ttft_ms\": ";
+            out += cfg::fmt_fixed(p.mean_ttft_ms, 3);
+            out += ",\n      \"mean_tpot_ms\": ";
+            out += cfg::fmt_fixed(p.mean_tpot_ms, 3);
+            out += "\n    }";
+        }
+    }
+    out += points.empty() ? "]\n}\n" : "\n  ]\n}\n";
     return out;
 }
 
-std::string sweep_summary_csv(const std::vector<SweepPoint>& points) {
+std::string assemble_summary_csv(const SummaryParts& parts, const std::vector<SweepPoint>& points) {
     std::string out = "point,failed,throughput_rps,mean_ttft_ms,mean_tpot_ms\n";
-    for (const auto& p : points) {
-        out += "\"" + p.point_id + "\"," + (p.failed ? "1" : "0") + ',';
-        out += cfg::fmt_fixed(p.mean_throughput_rps, 6) + ',' + cfg::fmt_fixed(p.mean_ttft_ms, 3) + ',' +
-               cfg::fmt_fixed(p.mean_tpot_ms, 3) + '\n';
+    for (size_t i = 0; i < points.size(); ++i) {
+        const SweepPoint& p = points[i];
+        out += parts.csv[i];
+        out += p.failed ? "1," : "0,";
+        out += cfg::fmt_fixed(p.mean_throughput_rps, 6);
+        out += ',';
+        out += cfg::fmt_fixed(p.mean_ttft_ms, 3);
+        out += ',';
+        out += cfg::fmt_fixed(p.mean_tpot_ms, 3);
+        out += '\n';
     }
     return out;
+}
+
+std::string sweep_summary_json(const std::vector<SweepPoint>& points) {
+    return assemble_summary_json(render_summary_prefixes(points), points);
+}
+
+std::string sweep_summary_csv(const std::vector<SweepPoint>& points) {
+    return assemble_summary_csv(render_summary_prefixes(points), points);
 }
 
 }  // namespace dsd::host

@@ -65,8 +65,18 @@ struct SweepTotals {
     double points = 0, replicas = 0, failed = 0, events = 0;
 };
 
+// Summary text split per point: the part known before the run (id and
+// assignment) and, once the points are filled in, the results.
+struct SummaryParts {
+    std::vector<std::string> json, csv;
+};
+SummaryParts render_summary_prefixes(const std::vector<SweepPoint>& points);
+std::string assemble_summary_json(const SummaryParts& parts, const std::vector<SweepPoint>& points);
+std::string assemble_summary_csv(const SummaryParts& parts, const std::vector<SweepPoint>& points);
+
 // run_sweep on the GPU; writes per-replica reports when out_dir is non-empty.
-SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir);
+// With `parts`, the summary prefixes are rendered while the kernels run.
+SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir, SummaryParts* parts = nullptr);
 std::string sweep_summary_json(const std::vector<SweepPoint>& points);
 std::string sweep_summary_csv(const std::vector<SweepPoint>& points);
 
