@@ -257,6 +257,24 @@ enum : uint32_t {
 };
 // Actions are kind | arg << 4 (args < 2^28: requests < 2^26, slots < 2^27).
 
+// Step kinds at which a lane's continuation chain stops and waits for the
+// warp's next vote.  The selected lanes run their chain (popping events as
+// they go) until they reach one of these, so the warp executes each of the
+// frequent, costly handlers - dispatch, iteration start, batch items, the
+// proposal and result arrivals - for all lanes that have it pending at once,
+// while the cheap or rare steps (pops, arrivals, prompt shipping, compute
+// completion, finish, activation) ride along inside the chains.  Making a
+// rare kind a barrier starves it: the vote picks the kind most lanes have
+// pending.  Measured on the C5 sweep (B200): {pop, dispatch} 170 ms, this set
+// 85 ms, every kind 210 ms.
+#ifndef DSD_BARRIER_KINDS
+#define DSD_BARRIER_KINDS                                                                            \
+    ((1u << kActDispatch) | (1u << kActBegin) | (1u << kActItem) | (1u << kActNetProposal) |         \
+     (1u << kActNetResult) | (1u << kActNone))
+#endif
+constexpr uint32_t kBarrierKinds = DSD_BARRIER_KINDS;
+DSD_HD bool is_barrier(uint32_t kind) { return (kBarrierKinds >> kind) & 1u; }
+
 struct Engine {
     // Register budget: everything below stays live across the whole event
     // loop, so only what nearly every step touches lives here; counters the
@@ -1085,6 +1103,10 @@ struct Engine {
     // events remain, else kActNone.  The kernel's warp scheduler reads it.
     DSD_HD uint32_t next_kind() const {
         if (fail) return kActNone;
+        return next_kind_unchecked();
+    }
+    // next_kind without the failure test (the kernel's chain loop tests it once per chain)
+    DSD_HD uint32_t next_kind_unchecked() const {
         if (sp > 0) return st0 & 15u;
         return (next_arr < N || heap_n > 0) ? static_cast<uint32_t>(kActPop) : static_cast<uint32_t>(kActNone);
     }
@@ -1157,7 +1179,8 @@ struct Engine {
     DSD_HD void step() {
         if (sp == 0) {
             pop_event();
-            return;
+            // a handler that is not a vote barrier runs in the same step
+            if (sp == 0 || is_barrier(st0 & 15u)) return;
         }
         const uint32_t a = pop_act();
         const uint32_t arg = a >> 4;

@@ -84,22 +84,7 @@ __host__ __device__ inline int64_t smem_warp_bytes(int64_t ns, int64_t heap_cap)
            (ns - 1) * kLanes * kHotStride;
 }
 
-// Step kinds at which a lane's continuation chain stops and waits for the
-// warp's next vote.  The selected lanes run their chain (popping events as
-// they go) until they reach one of these, so the warp executes each of the
-// frequent, costly handlers - dispatch, iteration start, batch items, the
-// proposal and result arrivals - for all lanes that have it pending at once,
-// while the cheap or rare steps (pops, arrivals, prompt shipping, compute
-// completion, finish, activation) ride along inside the chains.  Making a
-// rare kind a barrier starves it: the vote picks the kind most lanes have
-// pending.  Measured on the C5 sweep (B200): {pop, dispatch} 170 ms, this set
-// 85 ms, every kind 210 ms.
-#ifndef DSD_BARRIER_KINDS
-#define DSD_BARRIER_KINDS                                                                            \
-    ((1u << kActDispatch) | (1u << kActBegin) | (1u << kActItem) | (1u << kActNetProposal) |         \
-     (1u << kActNetResult) | (1u << kActNone))
-#endif
-constexpr uint32_t kBarrierKinds = DSD_BARRIER_KINDS;
+// kBarrierKinds (the vote barriers) is defined in engine.cuh.
 
 #ifndef DSD_VOTE_MODE
 #define DSD_VOTE_MODE 0
@@ -198,8 +183,9 @@ __global__ void __launch_bounds__(kBlock, DSD_MIN_BLOCKS) k_simulate(const __gri
                 } else {
                     e.step();
                 }
-                kind = e.next_kind();
+                kind = e.next_kind_unchecked();
             } while (!((kBarrierKinds >> kind) & 1u));
+            if (e.fail) kind = kActNone;  // a failed replica stops (checked once per chain)
         }
         if constexpr (kStats) ++iters;
     }
