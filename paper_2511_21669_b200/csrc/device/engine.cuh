@@ -98,34 +98,128 @@ DSD_HD_NOINLINE double grid_interpolate(const char* blob, const DevGrid& g, doub
 // with Backend::matvec in the AVX2 summation order the reference auto-selects
 // on AVX2 hosts (kernels_avx2.cpp:17-40, kernels_dispatch.cpp:21-26).
 // ---------------------------------------------------------------------------
-DSD_HD void matvec_avx2_order(const double* w, const double* x, const double* bias, double* y,
-                              int rows, int cols) {
+// one output row: 4 strided lane sums, hsum, scalar tail (the bias is added by the caller)
+DSD_HD double avx2_dot(const double* row, const double* x, int cols) {
     const int tail = cols & ~3;
-    for (int r = 0; r < rows; ++r) {
-        const double* row = w + static_cast<int64_t>(r) * cols;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int c = 0;
-        for (; c < tail; c += 4) {
-            a0 = a0 + row[c] * x[c];
-            a1 = a1 + row[c + 1] * x[c + 1];
-            a2 = a2 + row[c + 2] * x[c + 2];
-            a3 = a3 + row[c + 3] * x[c + 3];
-        }
-        double s = (a0 + a2) + (a1 + a3);  // hsum: lo+hi then unpackhi (kernels_avx2.cpp:17-23)
-        for (; c < cols; ++c) s += row[c] * x[c];
-        y[r] = bias[r] + s;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int c = 0;
+    for (; c < tail; c += 4) {
+        a0 = a0 + row[c] * x[c];
+        a1 = a1 + row[c + 1] * x[c + 1];
+        a2 = a2 + row[c + 2] * x[c + 2];
+        a3 = a3 + row[c + 3] * x[c + 3];
     }
+    double s = (a0 + a2) + (a1 + a3);  // hsum: lo+hi then unpackhi (kernels_avx2.cpp:17-23)
+    for (; c < cols; ++c) s += row[c] * x[c];
+    return s;
 }
 
-// out of line: ~34K flops per call, called once per AWC decision; keeping it
-// out of the event loop keeps the loop small enough for the instruction cache
-DSD_HD_NOINLINE double awc_predict(const char* blob, const DevScenario& S, const double raw[5]) {
-    double x[5];
+DSD_HD void matvec_avx2_order(const double* w, const double* x, const double* bias, double* y,
+                              int rows, int cols) {
+    for (int r = 0; r < rows; ++r) y[r] = bias[r] + avx2_dot(w + static_cast<int64_t>(r) * cols, x, cols);
+}
+
+// FeatureNormalizer::transform (mlp.cpp:163-170): raw features -> model input
+DSD_HD void awc_normalize(const DevScenario& S, const double raw[5], double x[5]) {
     for (int f = 0; f < 5; ++f) {
         double v = S.awc_log[f] ? log1p(raw[f]) : raw[f];
         double span = S.awc_hi[f] - S.awc_lo[f];
         x[f] = span > 0.0 ? (v - S.awc_lo[f]) / span : 0.0;
     }
+}
+
+// WcDnn::forward (mlp.cpp:83-97) by one thread on a normalised input
+DSD_HD_NOINLINE double awc_forward_lane(const char* blob, const DevScenario& S, const double* x);
+
+// Per-warp scratch of the cooperative AWC evaluation (shared memory): the
+// requesting lanes' model inputs and results, the request flags, and the
+// hidden vectors of the network being evaluated.
+struct AwcWarpScratch {
+    double x[kLanes][8];
+    double raw[kLanes];
+    double hv[kMaxHidden], sv[kMaxHidden];
+    int32_t req[kLanes];
+};
+
+#ifdef __CUDACC__
+// WcDnn::forward (mlp.cpp:83-97) of one lane's request, evaluated by the whole
+// warp: each output row is one lane's avx2_dot in the reference's order, so
+// the result is bit-identical to awc_predict; the vectors are broadcast
+// through shared memory.  Every lane of the warp must call it (converged).
+__device__ __noinline__ double awc_forward_warp(const char* blob, const DevScenario* S, const double* x,
+                                                AwcWarpScratch* sc) {
+    const int lane = threadIdx.x & (kLanes - 1);
+    const int H = S->awc_hidden, I = S->awc_input;
+    const double* p = blob_ptr<double>(blob, S->o_awc_params);
+    for (int r = lane; r < H; r += kLanes) sc->hv[r] = p[H * I + r] + avx2_dot(p + static_cast<int64_t>(r) * I, x, I);
+    __syncwarp();
+    int64_t off = static_cast<int64_t>(H) * I + H;
+    for (int b = 0; b < S->awc_blocks; ++b) {
+        const double* w1 = p + off;
+        const double* b1 = w1 + static_cast<int64_t>(H) * H;
+        const double* w2 = b1 + H;
+        const double* b2 = w2 + static_cast<int64_t>(H) * H;
+        for (int r = lane; r < H; r += kLanes) {
+            const double u = b1[r] + avx2_dot(w1 + static_cast<int64_t>(r) * H, sc->hv, H);
+            const double sg = 1.0 / (1.0 + exp(-u));  // kernels::silu (kernels_scalar.cpp:65-70)
+            sc->sv[r] = u * sg;
+        }
+        __syncwarp();
+        for (int r = lane; r < H; r += kLanes) sc->hv[r] += b2[r] + avx2_dot(w2 + static_cast<int64_t>(r) * H, sc->sv, H);
+        __syncwarp();
+        off += 2 * static_cast<int64_t>(H) * H + 2 * H;
+    }
+    double out = 0.0;
+    if (lane == 0) {
+        const double* w_out = p + off;
+        out = w_out[H];  // b_out, then the sequential head (mlp.cpp:93-95)
+        for (int i = 0; i < H; ++i) out += w_out[i] * sc->hv[i];
+    }
+    __syncwarp();
+    return __shfl_sync(0xffffffffu, out, 0);
+}
+
+// Serves every pending AWC request of the warp.  A few requests (a sparse or
+// single-replica batch) are evaluated one at a time by all 32 lanes (idle and
+// finished lanes included); many requests at once are faster as one
+// evaluation per requesting lane, in parallel.
+constexpr int kAwcCoopMax = 6;
+__device__ __forceinline__ void awc_serve_warp(const char* blob, const DevScenario* my_scen, AwcWarpScratch* sc) {
+    const int lane = threadIdx.x & (kLanes - 1);
+    unsigned pending = __ballot_sync(0xffffffffu, sc->req[lane] != 0);
+    if (__popc(pending) > kAwcCoopMax) {
+        if (sc->req[lane]) {
+            sc->raw[lane] = awc_forward_lane(blob, *my_scen, sc->x[lane]);
+            sc->req[lane] = 0;
+        }
+        __syncwarp();
+        return;
+    }
+    while (pending) {
+        const int src = __ffs(pending) - 1;
+        pending &= pending - 1;
+        const DevScenario* S = reinterpret_cast<const DevScenario*>(
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_scen), src));
+        const double raw = awc_forward_warp(blob, S, sc->x[src], sc);
+        if (lane == src) {
+            sc->raw[lane] = raw;
+            sc->req[lane] = 0;
+        }
+        __syncwarp();
+    }
+}
+#endif
+
+// out of line: ~34K flops per call, called once per AWC decision; keeping it
+// out of the event loop keeps the loop small enough for the instruction cache
+DSD_HD double awc_predict(const char* blob, const DevScenario& S, const double raw[5]) {
+    double x[5];
+    awc_normalize(S, raw, x);
+    return awc_forward_lane(blob, S, x);
+}
+
+// WcDnn::forward (mlp.cpp:83-97) by one thread on a normalised input
+DSD_HD_NOINLINE double awc_forward_lane(const char* blob, const DevScenario& S, const double* x) {
     const int H = S.awc_hidden, I = S.awc_input;
     const double* p = blob_ptr<double>(blob, S.o_awc_params);
     double h[kMaxHidden], u[kMaxHidden], s[kMaxHidden];
@@ -252,7 +346,8 @@ enum : uint32_t {
     kActActivate = 9,     // activate_next_session(d)          arg = d
     kActDispatch = 10,    // try_dispatch(v, expired)          arg = v*2 + expired
     kActSendPrompt = 11,  // ship the prompt to the verifier   arg = i
-    kActKinds = 12,
+    kActBeginAwc = 12,    // AWC decision served -> begin       arg = i
+    kActKinds = 13,
     kActNone = 15         // replica finished
 };
 // Actions are kind | arg << 4 (args < 2^28: requests < 2^26, slots < 2^27).
@@ -270,7 +365,7 @@ enum : uint32_t {
 #ifndef DSD_BARRIER_KINDS
 #define DSD_BARRIER_KINDS                                                                            \
     ((1u << kActDispatch) | (1u << kActBegin) | (1u << kActItem) | (1u << kActNetProposal) |         \
-     (1u << kActNetResult) | (1u << kActNone))
+     (1u << kActNetResult) | (1u << kActBeginAwc) | (1u << kActNone))
 #endif
 constexpr uint32_t kBarrierKinds = DSD_BARRIER_KINDS;
 DSD_HD bool is_barrier(uint32_t kind) { return (kBarrierKinds >> kind) & 1u; }
@@ -331,10 +426,13 @@ struct Engine {
     // prefill / decode-shaped) and the link's one-way delay, resolved once
     const DevGrid *g_tp = nullptr, *g_td = nullptr, *g_dp = nullptr, *g_dd = nullptr;
     int64_t link_us = 0;
+    // the warp's cooperative AWC scratch (shared memory), null for batches
+    // without AWC scenarios (decisions then run awc_predict on the lane)
+    AwcWarpScratch* awc = nullptr;
 
     DSD_HD Engine(const Workspace& w, const DevScenario& s, int64_t replica, int32_t* server_base,
                   int64_t* heap_time_base, uint64_t* heap_key_base, int64_t heap_cap, int32_t server_cap,
-                  unsigned char* hot_base = nullptr, bool specialized = false)
+                  unsigned char* hot_base = nullptr, bool specialized = false, AwcWarpScratch* awc_scratch = nullptr)
         : W(w), S(s), rep(static_cast<int32_t>(replica)), sb(server_base), htb(heap_time_base),
           hkb(heap_key_base), hcap(static_cast<int32_t>(heap_cap)), nsc(server_cap), spec(specialized) {
         R = W.req + replica * W.c.nr;
@@ -359,6 +457,7 @@ struct Engine {
         T = S.n_targets;
         D = S.n_drafts;
         hotb = S.fused_everything ? nullptr : hot_base;
+        awc = awc_scratch;
         pflags = static_cast<uint32_t>(S.fused_everything) | (static_cast<uint32_t>(S.pair_stats) << 1) |
                  (static_cast<uint32_t>(S.batching == 1) << 2) | (static_cast<uint32_t>(S.jitter_free) << 3) |
                  (static_cast<uint32_t>(S.window_kind) << 4) | (static_cast<uint32_t>(S.routing) << 6) |
@@ -624,42 +723,45 @@ struct Engine {
                 int64_t p = pair_of(d, t);
                 double f[5];
                 extract_features(W, rep, p, t, SV(v_open, t), S.queue_capacity, link(d, t).rtt_ms, f);
-                double raw = awc_predict(W.blob, S, f);
-                // stabilized_decide (smoother.cpp:8-37)
-                const double gmin = static_cast<double>(S.gamma_min);
-                const double gmax = static_cast<double>(S.gamma_max);
-                double clamped = raw < gmin ? gmin : (gmax < raw ? gmax : raw);
-                uint8_t& init = IL(W.p_sm_init, W.c.np, p);
-                double& ema = IL(W.p_sm_ema, W.c.np, p);
-                int32_t& low = IL(W.p_sm_low, W.c.np, p);
-                uint8_t& fz = IL(W.p_sm_fused, W.c.np, p);
-                const double ema_alpha = 0.4;
-                if (!init) {
-                    ema = clamped;
-                    init = 1;
-                } else {
-                    ema = ema_alpha * clamped + (1.0 - ema_alpha) * ema;
-                }
-                if (!fz) {
-                    if (ema <= 1.5) {
-                        ++low;
-                    } else {
-                        low = 0;
-                    }
-                    if (low >= 2) fz = 1;
-                } else if (ema > 1.5) {
-                    fz = 0;
-                    low = 0;
-                }
-                int g = static_cast<int>(floor(ema + 0.5));
-                int gi_min = static_cast<int>(gmin), gi_max = static_cast<int>(gmax);
-                g = g < gi_min ? gi_min : (gi_max < g ? gi_max : g);
-                if (fz && g <= 1) return Decision{true, 1};
-                return Decision{false, g > 1 ? g : 1};
+                return stabilized_decide(p, awc_predict(W.blob, S, f));
             }
             default:
                 return Decision{true, 1};
         }
+    }
+    // stabilized_decide (smoother.cpp:8-37) of the pair's smoother on a raw
+    // AWC prediction
+    DSD_HD Decision stabilized_decide(int64_t p, double raw) {
+        const double gmin = static_cast<double>(S.gamma_min);
+        const double gmax = static_cast<double>(S.gamma_max);
+        double clamped = raw < gmin ? gmin : (gmax < raw ? gmax : raw);
+        uint8_t& init = IL(W.p_sm_init, W.c.np, p);
+        double& ema = IL(W.p_sm_ema, W.c.np, p);
+        int32_t& low = IL(W.p_sm_low, W.c.np, p);
+        uint8_t& fz = IL(W.p_sm_fused, W.c.np, p);
+        const double ema_alpha = 0.4;
+        if (!init) {
+            ema = clamped;
+            init = 1;
+        } else {
+            ema = ema_alpha * clamped + (1.0 - ema_alpha) * ema;
+        }
+        if (!fz) {
+            if (ema <= 1.5) {
+                ++low;
+            } else {
+                low = 0;
+            }
+            if (low >= 2) fz = 1;
+        } else if (ema > 1.5) {
+            fz = 0;
+            low = 0;
+        }
+        int g = static_cast<int>(floor(ema + 0.5));
+        int gi_min = static_cast<int>(gmin), gi_max = static_cast<int>(gmax);
+        g = g < gi_min ? gi_min : (gi_max < g ? gi_max : g);
+        if (fz && g <= 1) return Decision{true, 1};
+        return Decision{false, g > 1 ? g : 1};
     }
 
     // ---- work queues: intrusive lists through the records' item slots ----
@@ -898,7 +1000,32 @@ struct Engine {
 
     // [decide_window] + begin_iteration (engine.cpp:254-257, 383-404)
     DSD_HD void begin(int64_t i, bool decide) {
-        Decision dec = decide ? decide_window(i) : Decision{true, 1};
+        if (decide && awc && wkind() == 2) {
+            const ReqRec& r = rec(i);
+            const int32_t d = D > 0 ? r.drafter : -1;
+            if (d >= 0) {
+                // AWC decision: park the model input and yield; the warp
+                // evaluates the network cooperatively (awc_serve_warp) before
+                // the continuation kActBeginAwc runs the smoother and the rest
+                const int32_t t = r.target;
+                double f[5];
+                extract_features(W, rep, pair_of(d, t), t, SV(v_open, t), S.queue_capacity, link(d, t).rtt_ms, f);
+                const int lane = rep & 31;
+                awc_normalize(S, f, awc->x[lane]);
+                awc->req[lane] = 1;
+                push_act(act(kActBeginAwc, static_cast<uint32_t>(i)));
+                return;
+            }
+        }
+        begin_with(i, decide ? decide_window(i) : Decision{true, 1});
+    }
+    // continuation of begin once the warp served the AWC request
+    DSD_HD void begin_awc(int64_t i) {
+        const ReqRec& r = rec(i);
+        const Decision dec = stabilized_decide(pair_of(r.drafter, r.target), awc->raw[rep & 31]);
+        begin_with(i, dec);
+    }
+    DSD_HD void begin_with(int64_t i, const Decision& dec) {
         ReqRec& r = rec(i);
         if (phase(r) == kPhDone) return;
         int32_t d = D > 0 ? r.drafter : -1;
@@ -1167,6 +1294,9 @@ struct Engine {
                 break;
             }
             case kActArrival: on_arrival(arg); break;
+            case kActBeginAwc:
+                if (!spec) begin_awc(arg);  // (no AWC in the specialised kernel)
+                break;
             default: {  // kActNetPrompt: on_net_arrive (engine.cpp:406-435)
                 const ReqRec& r = rec(arg);
                 enqueue(r.target, arg, 0, kOpPrefill, r.prompt, true);

@@ -103,6 +103,7 @@ struct Caps {
     int64_t bw;      // acceptance-bit words per replica
     int64_t n;       // replicas
     int64_t nwarps;  // ceil(n / 32)
+    int64_t awc;     // some scenario decides windows with the AWC model (cooperative scratch needed)
 };
 
 struct DevSummary {  // == dsd_replica_summary

@@ -232,6 +232,7 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
             }
         }
         if (d.pair_stats) any_pairs = true;
+        if (d.window_kind == DSD_WINDOW_AWC && !d.fused_everything) c.awc = 1;
         // workload
         d.workload = s.workload;
         int64_t N = 0, bw = 0, lbound = 0;

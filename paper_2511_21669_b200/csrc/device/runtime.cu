@@ -79,9 +79,9 @@ __global__ void __launch_bounds__(kBlock) k_stage(Workspace W, int64_t* ltot, co
 // Shared memory per warp of the kSmem variant: server fields, heap slots, the
 // active-session record slots (one per possible draft server, ns - 1) and
 // their first acceptance-bit words.
-__host__ __device__ inline int64_t smem_warp_bytes(int64_t ns, int64_t heap_cap) {
+__host__ __device__ inline int64_t smem_warp_bytes(int64_t ns, int64_t heap_cap, bool awc) {
     return static_cast<int64_t>(kServerFields) * ns * kLanes * 4 + heap_cap * kLanes * 16 +
-           (ns - 1) * kLanes * kHotStride;
+           (ns - 1) * kLanes * kHotStride + (awc ? static_cast<int64_t>(sizeof(AwcWarpScratch)) : 0);
 }
 
 // kBarrierKinds (the vote barriers) is defined in engine.cuh.
@@ -119,7 +119,9 @@ __device__ __forceinline__ uint32_t vote_kind(unsigned best) {
 #define DSD_MIN_BLOCKS 8
 #endif
 // kSpec: the single-pair specialisation (Engine::spec; kSmem only).
-template <bool kSmem, bool kStats, bool kSpec = false>
+// kAwc: the batch has AWC scenarios (cooperative AWC scratch + serving); the
+// other instantiations compile that code out.
+template <bool kSmem, bool kStats, bool kSpec = false, bool kAwc = false>
 __global__ void __launch_bounds__(kBlock, DSD_MIN_BLOCKS) k_simulate(const __grid_constant__ Workspace W,
                                                                       const int32_t* list, const int32_t* count,
                                                      int32_t smem_heap_cap) {
@@ -132,17 +134,21 @@ __global__ void __launch_bounds__(kBlock, DSD_MIN_BLOCKS) k_simulate(const __gri
     int64_t hcap;
     int32_t nsc;
     unsigned char* hot = nullptr;
+    AwcWarpScratch* awc = nullptr;
+    extern __shared__ __align__(16) unsigned char smem[];
     if constexpr (kSmem) {
-        extern __shared__ __align__(16) unsigned char smem[];
         const int lane = threadIdx.x % kLanes;
         nsc = kSpec ? 2 : static_cast<int32_t>(W.c.ns);
         hcap = smem_heap_cap;
         const int64_t srv_bytes = static_cast<int64_t>(kServerFields) * nsc * kLanes * 4;
-        unsigned char* blk = smem + (threadIdx.x / kLanes) * smem_warp_bytes(nsc, hcap);
+        constexpr bool with_awc = kAwc;
+        unsigned char* blk = smem + (threadIdx.x / kLanes) * smem_warp_bytes(nsc, hcap, with_awc);
         sbase = reinterpret_cast<int32_t*>(blk) + lane;
         hb = reinterpret_cast<int64_t*>(blk + srv_bytes) + lane;
         kb = reinterpret_cast<uint64_t*>(blk + srv_bytes + hcap * kLanes * 8) + lane;
         hot = blk + srv_bytes + hcap * kLanes * 16 + lane * kHotStride;
+        if (with_awc)
+            awc = reinterpret_cast<AwcWarpScratch*>(blk + srv_bytes + hcap * kLanes * 16 + (nsc - 1) * kLanes * kHotStride);
     } else {
         const int64_t w = r / kLanes, lane = r % kLanes;
         nsc = static_cast<int32_t>(W.c.ns);
@@ -150,8 +156,10 @@ __global__ void __launch_bounds__(kBlock, DSD_MIN_BLOCKS) k_simulate(const __gri
         sbase = W.srv + w * kServerFields * W.c.ns * kLanes + lane;
         hb = W.h_time + w * W.c.hc * kLanes + lane;
         kb = W.h_key + w * W.c.hc * kLanes + lane;
+        if constexpr (kAwc) awc = reinterpret_cast<AwcWarpScratch*>(smem) + threadIdx.x / kLanes;
     }
-    Engine e(W, W.scen[W.rep_scen[r]], r, sbase, hb, kb, hcap, nsc, hot, kSpec);
+    if constexpr (kAwc) awc->req[threadIdx.x % kLanes] = 0;
+    Engine e(W, W.scen[W.rep_scen[r]], r, sbase, hb, kb, hcap, nsc, hot, kSpec, awc);
     if (live) e.init();
     uint32_t kind = live ? e.next_kind() : static_cast<uint32_t>(kActNone);
     // kStats: per-step-kind cycle profile (DSD_STEP_STATS=1), one block-level
@@ -165,6 +173,9 @@ __global__ void __launch_bounds__(kBlock, DSD_MIN_BLOCKS) k_simulate(const __gri
         t_start = clock64();
     }
     for (;;) {
+        // AWC decisions requested during the last chains: the whole warp
+        // evaluates each requester's network (warp-uniform branch)
+        if constexpr (kAwc) awc_serve_warp(W.blob, &e.S, awc);
         // the kind most lanes have pending (majority vote)
         const unsigned peers = __match_any_sync(0xffffffffu, kind);
         const unsigned score = kind == kActNone ? 0u : vote_score(static_cast<unsigned>(__popc(peers)), kind);
@@ -426,6 +437,8 @@ void Runtime::launch() {
         return;
     }
     const unsigned grid = static_cast<unsigned>((R.n + kBlock - 1) / kBlock);
+    // the HBM variant's only shared memory: the cooperative AWC scratch
+    const size_t hbm_smem = R.W.c.awc ? (kBlock / kLanes) * sizeof(AwcWarpScratch) : 0;
     DSD_CUDA(cudaEventRecord(R.ev[0], R.stream));
     k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, R.collect ? static_cast<int64_t*>(R.ltot.p) : nullptr, nullptr,
                                            nullptr);
@@ -459,7 +472,7 @@ void Runtime::launch() {
     DSD_CUDA(cudaEventRecord(R.ev[1], R.stream));
     const bool smem = R.W.c.ns <= kSmemServers && R.smem_heap > 0;
     if (smem) {
-        const size_t bytes = static_cast<size_t>(kBlock / kLanes) * smem_warp_bytes(R.W.c.ns, R.smem_heap);
+        const size_t bytes = static_cast<size_t>(kBlock / kLanes) * smem_warp_bytes(R.W.c.ns, R.smem_heap, R.W.c.awc != 0);
         // Carveout: just the shared memory of the blocks one wave puts on an
         // SM (1 KB of it reserved per block); the rest of the 256 KB array is
         // L1.  The driver's default sizes for the launch-bounds maximum (8
@@ -471,12 +484,17 @@ void Runtime::launch() {
             pct = static_cast<int>(std::min<int64_t>(100, (100 * need + R.smem_per_sm - 1) / R.smem_per_sm));
         }
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         const bool spec = R.spec_ok && R.specialize && !R.collect && !R.W.probe;
         if (spec)
             (R.step_stats ? k_simulate<true, true, true> : k_simulate<true, false, true>)<<<grid, kBlock, bytes, R.stream>>>(
+                R.W, nullptr, nullptr, R.smem_heap);
+        else if (R.W.c.awc)
+            (R.step_stats ? k_simulate<true, true, false, true> : k_simulate<true, false, false, true>)<<<grid, kBlock, bytes,
+                                                                                                    R.stream>>>(
                 R.W, nullptr, nullptr, R.smem_heap);
         else
             (R.step_stats ? k_simulate<true, true> : k_simulate<true, false>)<<<grid, kBlock, bytes, R.stream>>>(
@@ -491,11 +509,13 @@ void Runtime::launch() {
         k_collect_overflow<<<g2, 256, 0, R.stream>>>(R.W, list, count);
         k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, R.collect ? static_cast<int64_t*>(R.ltot.p) : nullptr, list,
                                                 count);
-        (R.step_stats ? k_simulate<false, true> : k_simulate<false, false>)<<<grid, kBlock, 0, R.stream>>>(R.W, list, count, 0);
+        (R.W.c.awc ? (R.step_stats ? k_simulate<false, true, false, true> : k_simulate<false, false, false, true>)
+                    : (R.step_stats ? k_simulate<false, true> : k_simulate<false, false>))<<<grid, kBlock, hbm_smem, R.stream>>>(R.W, list, count, 0);
         DSD_CUDA(cudaGetLastError());
         R.launches += 4;
     } else {
-        (R.step_stats ? k_simulate<false, true> : k_simulate<false, false>)<<<grid, kBlock, 0, R.stream>>>(R.W, nullptr, nullptr, 0);
+        (R.W.c.awc ? (R.step_stats ? k_simulate<false, true, false, true> : k_simulate<false, false, false, true>)
+                    : (R.step_stats ? k_simulate<false, true> : k_simulate<false, false>))<<<grid, kBlock, hbm_smem, R.stream>>>(R.W, nullptr, nullptr, 0);
         DSD_CUDA(cudaGetLastError());
         ++R.launches;
     }
