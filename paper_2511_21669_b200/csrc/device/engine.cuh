@@ -794,6 +794,7 @@ struct Engine {
     // try_dispatch (engine.cpp:485-567)
     DSD_HD void try_dispatch(int32_t v, bool window_expired) {
         if (busy(v) || SV(v_qhead, v) < 0) return;
+        if (spec && v == 1 && dispatch_single_draft()) return;
         const bool is_draft = v >= T;
         const int64_t mb = is_draft ? dmax_batch : max_batch;
         int32_t kind = -1;
@@ -905,6 +906,36 @@ struct Engine {
         set_busy_flag(v, true);
         if (!is_draft) set_busy(v, get_busy(v) + lat);  // only target busy time is reported
         defer(now + lat, info(kEvComputeDone, 0, static_cast<uint32_t>(v)));
+    }
+
+    // try_dispatch of the specialised kernel's draft server when its queue
+    // holds one item (the active session's draft prefill or decode): the
+    // general forming pass below reduces to taking that item (always
+    // eligible, never via the network); same latency query and rounding.
+    DSD_HD bool dispatch_single_draft() {
+        const int32_t cur = SV(v_qhead, 1);
+        ReqRec& r = rec(cur >> 1);
+        const int k = cur & 1;
+        if (r.next[k] >= 0) return false;  // more than one item: the general path
+        const uint32_t op = r.op[k] & 3u;
+        SV(v_qhead, 1) = -1;
+        SV(v_qtail, 1) = -1;
+        SV(v_run, 1) = cur;
+        const int32_t t_i = k ? r.tok1 : r.prompt;
+        const int32_t tok = t_i > 1 ? t_i : 1;
+        const bool prefill = op == kOpPrefill;
+        const int64_t ctx = prefill ? 0 : static_cast<int64_t>(r.prompt) + r.tokens;
+        // qb = taken = 1 (prefill / decode); qc = prompt tokens / context
+        const DevGrid& g = *(prefill ? g_dp : g_dd);
+        const int64_t qc = prefill ? static_cast<int64_t>(tok) : (ctx > 0 ? ctx : 0);
+        double ms = g.o_btab >= 0 && g.o_ctab >= 0 ? grid_interpolate_int(W.blob, g, 1, qc)
+                                                    : grid_interpolate(W.blob, g, 1.0, static_cast<double>(qc));
+        if (!prefill) ms *= tok;  // decode: latency x tokens_per_request
+        int64_t lat = llround(ms * 1000.0);
+        if (lat < 1) lat = 1;
+        set_busy_flag(1, true);
+        defer(now + lat, info(kEvComputeDone, 0, 1u));
+        return true;
     }
 
     // ---- request lifecycle ----
