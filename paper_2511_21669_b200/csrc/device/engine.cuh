@@ -466,6 +466,15 @@ struct Engine {
                  (static_cast<uint32_t>(S.batching_window_us > 0) << 10);
     }
     DSD_HD bool hot() const { return spec || hotb != nullptr; }
+    // this thread's lane in its warp (per-warp shared-memory slots); a
+    // replica's index says nothing about it when the kernel runs a replica list
+    static DSD_HD int hw_lane() {
+#ifdef __CUDA_ARCH__
+        return static_cast<int>(threadIdx.x & (kLanes - 1));
+#else
+        return 0;
+#endif
+    }
     DSD_HD bool collecting() const { return !spec && W.collect; }
     DSD_HD bool probing() const { return !spec && W.probe != nullptr; }
     DSD_HD bool fe() const { return pflags & 1u; }
@@ -1041,7 +1050,7 @@ struct Engine {
                 const int32_t t = r.target;
                 double f[5];
                 extract_features(W, rep, pair_of(d, t), t, SV(v_open, t), S.queue_capacity, link(d, t).rtt_ms, f);
-                const int lane = rep & 31;
+                const int lane = hw_lane();
                 awc_normalize(S, f, awc->x[lane]);
                 awc->req[lane] = 1;
                 push_act(act(kActBeginAwc, static_cast<uint32_t>(i)));
@@ -1053,7 +1062,7 @@ struct Engine {
     // continuation of begin once the warp served the AWC request
     DSD_HD void begin_awc(int64_t i) {
         const ReqRec& r = rec(i);
-        const Decision dec = stabilized_decide(pair_of(r.drafter, r.target), awc->raw[rep & 31]);
+        const Decision dec = stabilized_decide(pair_of(r.drafter, r.target), awc->raw[hw_lane()]);
         begin_with(i, dec);
     }
     DSD_HD void begin_with(int64_t i, const Decision& dec) {

@@ -38,10 +38,10 @@ constexpr int kBlock = 64;
 // the overflow re-run covers the `*count` replicas in `list`.
 __device__ __forceinline__ bool replica_of(const Workspace& W, const int32_t* list, const int32_t* count,
                                           int64_t t, int64_t& rep) {
-    if (list) {
+    if (list) {  // a replica list (overflow re-run, lane placement); -1 = an idle lane
         if (t >= *count) return false;
         rep = list[t];
-        return true;
+        return rep >= 0;
     }
     rep = t;
     return t < W.c.n;
@@ -118,11 +118,16 @@ __device__ __forceinline__ uint32_t vote_kind(unsigned best) {
 #ifndef DSD_MIN_BLOCKS
 #define DSD_MIN_BLOCKS 8
 #endif
+// the specialised kernel needs ~100 registers: more resident blocks per SM
+// leave room for thin warps (placement_list) in one wave
+#ifndef DSD_SPEC_MIN_BLOCKS
+#define DSD_SPEC_MIN_BLOCKS 10
+#endif
 // kSpec: the single-pair specialisation (Engine::spec; kSmem only).
 // kAwc: the batch has AWC scenarios (cooperative AWC scratch + serving); the
 // other instantiations compile that code out.
 template <bool kSmem, bool kStats, bool kSpec = false, bool kAwc = false>
-__global__ void __launch_bounds__(kBlock, DSD_MIN_BLOCKS) k_simulate(const __grid_constant__ Workspace W,
+__global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_BLOCKS) k_simulate(const __grid_constant__ Workspace W,
                                                                       const int32_t* list, const int32_t* count,
                                                      int32_t smem_heap_cap) {
     int64_t rep = 0;
@@ -282,6 +287,12 @@ struct RuntimeImpl {
     // shared-memory carveout of the kSmem kernels (% of the SM's maximum):
     // -1 = sized per launch (Runtime::launch), env DSD_CARVEOUT fixes it
     int carveout = -1;
+    // lane placement of the simulation kernel: [count][thread -> replica or
+    // -1] (empty: replica = thread index)
+    DevBuf place;
+    int64_t place_n = 0;
+    int lanes_per_warp = 32;  // env DSD_LANES_PER_WARP: replicas per warp (experiments)
+    bool placement = true;    // cost-aware lane placement (env DSD_PLACEMENT=0 disables)
     int sms = 148, smem_per_sm = 228 * 1024;
     DevBuf stats;
     Workspace W{};
@@ -317,6 +328,9 @@ Runtime::Runtime(int device) : impl_(new RuntimeImpl) {
     if (const char* h = std::getenv("DSD_SMEM_HEAP")) impl_->smem_heap = std::max(0, std::atoi(h));
     if (const char* s = std::getenv("DSD_STEP_STATS")) impl_->step_stats = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_SPECIALIZE")) impl_->specialize = std::atoi(s) != 0;
+    if (const char* s = std::getenv("DSD_PLACEMENT")) impl_->placement = std::atoi(s) != 0;
+    if (const char* s = std::getenv("DSD_LANES_PER_WARP"))
+        impl_->lanes_per_warp = std::max(1, std::min(kLanes, std::atoi(s)));
     if (const char* s = std::getenv("DSD_CARVEOUT")) {  // shared-memory share of the L1/smem array (%)
         impl_->carveout = std::atoi(s);
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -342,6 +356,74 @@ size_t Runtime::replica_count() const { return impl_->n; }
 void Runtime::transfer_bytes(int64_t* h2d, int64_t* d2h) const {
     if (h2d) *h2d = impl_->h2d_bytes;
     if (d2h) *d2h = impl_->d2h_bytes;
+}
+
+// Cost-aware lane placement: a warp advances at the pace of its
+// slowest lane, and a warp with fewer live lanes needs fewer vote rounds, so
+// the heaviest replicas get warps of 8 or 16 live lanes and the rest full
+// warps, as long as all warps stay resident in one wave (`warp_cap`).
+// Replicas are sorted by an estimate of their event count - for a
+// synthetic workload with a static window, N x (4 + 5 x median output /
+// E[tokens per round]) with E[tokens per round] = (1 - a^(g+1)) / (1 - a)
+// (the speculative-decoding expectation) - so warps are also homogeneous.
+// Returns [count][thread -> replica or -1], or nothing when every replica
+// looks alike or the batch already needs more than one wave.  Placement only
+// chooses which thread runs which replica: results are unchanged.
+static std::vector<int32_t> placement_list(const Packed& P, size_t n, int64_t warp_cap) {
+    if (n < 2 * kLanes) return {};
+    const int64_t dense = (static_cast<int64_t>(n) + kLanes - 1) / kLanes;
+    if (dense >= warp_cap) return {};
+    std::vector<double> est(P.scen.size(), 0.0);
+    for (size_t k = 0; k < P.scen.size(); ++k) {
+        const DevScenario& d = P.scen[k];
+        if (d.workload != 0 || d.n_drafts < 1 || d.fused_everything || d.window_kind != 0) return {};
+        const double a = d.alpha, g = d.gamma;
+        const double tau = a < 1.0 ? (1.0 - std::pow(a, g + 1.0)) / (1.0 - a) : g + 1.0;
+        est[k] = static_cast<double>(d.n_requests) * (4.0 + 5.0 * std::exp(d.o_mu) / tau);
+    }
+    std::vector<int32_t> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+        return est[P.rep_scen[static_cast<size_t>(x)]] > est[P.rep_scen[static_cast<size_t>(y)]];
+    });
+    const double top = est[P.rep_scen[static_cast<size_t>(order[0])]];
+    if (!(top > 1.05 * est[P.rep_scen[static_cast<size_t>(order[n - 1])]])) return {};
+    // tiers: >= 85% of the heaviest -> 8 lanes, >= 70% -> 16 lanes, rest 32;
+    // shrink the thin tiers until the warps fit one wave
+    static const double th8 = std::getenv("DSD_PLACE_T8") ? std::atof(std::getenv("DSD_PLACE_T8")) : 0.90;
+    static const double th16 = std::getenv("DSD_PLACE_T16") ? std::atof(std::getenv("DSD_PLACE_T16")) : 0.75;
+    int64_t t8 = 0, t16 = 0;
+    for (size_t i = 0; i < n; ++i) {
+        const double e = est[P.rep_scen[static_cast<size_t>(order[i])]];
+        if (e >= th8 * top) ++t8; else if (e >= th16 * top) ++t16;
+    }
+    auto warps = [&](int64_t a8, int64_t a16) {
+        return (a8 + 7) / 8 + (a16 + 15) / 16 + (static_cast<int64_t>(n) - a8 - a16 + kLanes - 1) / kLanes;
+    };
+    while (warps(t8, t16) > warp_cap && (t8 > 0 || t16 > 0)) {
+        if (t8 > 0) {
+            const int64_t m = std::min<int64_t>(t8, 8);
+            t8 -= m;
+            t16 += m;
+        } else {
+            t16 -= std::min<int64_t>(t16, 16);
+        }
+    }
+    if (t8 == 0 && t16 == 0) return {};
+    std::vector<int32_t> pl(1, 0);
+    size_t i = 0;
+    auto emit = [&](int64_t count, int lanes) {
+        for (int64_t done = 0; done < count;) {
+            for (int l = 0; l < kLanes; ++l)
+                pl.push_back(l < lanes && done < count ? order[i + static_cast<size_t>(done++)] : -1);
+        }
+        i += static_cast<size_t>(count);
+    };
+    emit(t8, 8);
+    emit(t16, 16);
+    emit(static_cast<int64_t>(n) - t8 - t16, kLanes);
+    pl[0] = static_cast<int32_t>(pl.size() - 1);
+    return pl;
 }
 
 void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n,
@@ -411,11 +493,33 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
         R.probe.ensure(sizeof(double) * kProbeFields * std::max<size_t>(n, 1));
         W.probe = static_cast<double*>(R.probe.p);
     }
+    // lane placement
+    R.place_n = 0;
     R.spec_ok = c.ns == 2;
     for (const DevScenario& d : P.scen)
         R.spec_ok = R.spec_ok && d.n_targets == 1 && d.n_drafts == 1 && !d.fused_everything && d.window_kind == 0 &&
                     d.batching == 0 && d.batching_window_us == 0 && d.jitter_free && d.n_dg == 1 && d.n_tg == 1 &&
                     !d.has_order && !d.pair_stats;
+    const bool spec_launch = R.spec_ok && R.specialize && !collect && !feature_probe;
+    const int64_t max_blocks = spec_launch ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_BLOCKS;
+    std::vector<int32_t> pl = placement_list(P, n, R.sms * max_blocks * (kBlock / kLanes));
+    if (!pl.empty() && R.placement && R.lanes_per_warp == kLanes) {
+        R.place.ensure(4 * pl.size());
+        DSD_CUDA(cudaMemcpyAsync(R.place.p, pl.data(), 4 * pl.size(), cudaMemcpyHostToDevice, R.stream));
+        R.place_n = static_cast<int64_t>(pl.size()) - 1;
+    }
+    if (R.lanes_per_warp < kLanes && n > 0) {
+        const int64_t lpw = R.lanes_per_warp;
+        const int64_t nw = (static_cast<int64_t>(n) + lpw - 1) / lpw;
+        std::vector<int32_t> pl(static_cast<size_t>(nw * kLanes + 1), -1);
+        pl[0] = static_cast<int32_t>(nw * kLanes);
+        for (int64_t w = 0; w < nw; ++w)
+            for (int64_t l = 0; l < lpw; ++l)
+                if (w * lpw + l < static_cast<int64_t>(n)) pl[1 + w * kLanes + l] = static_cast<int32_t>(w * lpw + l);
+        R.place.ensure(4 * pl.size());
+        DSD_CUDA(cudaMemcpyAsync(R.place.p, pl.data(), 4 * pl.size(), cudaMemcpyHostToDevice, R.stream));
+        R.place_n = nw * kLanes;
+    }
     R.host_scen = std::move(P.scen);
     R.n = n;
     R.collect = collect;
@@ -473,13 +577,17 @@ void Runtime::launch() {
     const bool smem = R.W.c.ns <= kSmemServers && R.smem_heap > 0;
     if (smem) {
         const size_t bytes = static_cast<size_t>(kBlock / kLanes) * smem_warp_bytes(R.W.c.ns, R.smem_heap, R.W.c.awc != 0);
+        const int32_t* pcount = R.place_n ? static_cast<const int32_t*>(R.place.p) : nullptr;
+        const int32_t* plist = R.place_n ? pcount + 1 : nullptr;
+        const unsigned sgrid = R.place_n ? static_cast<unsigned>((R.place_n + kBlock - 1) / kBlock) : grid;
+        const bool spec = R.spec_ok && R.specialize && !R.collect && !R.W.probe;
         // Carveout: just the shared memory of the blocks one wave puts on an
         // SM (1 KB of it reserved per block); the rest of the 256 KB array is
         // L1.  The driver's default sizes for the launch-bounds maximum (8
         // blocks) even when 65,536 replicas need 7 per SM, costing 32-64 KB of L1.
         int pct = R.carveout;
         if (pct < 0) {
-            const int64_t per_sm = std::min<int64_t>(DSD_MIN_BLOCKS, (grid + R.sms - 1) / R.sms);
+            const int64_t per_sm = std::min<int64_t>(spec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_BLOCKS, (sgrid + R.sms - 1) / R.sms);
             const int64_t need = per_sm * (static_cast<int64_t>(bytes) + 1024);
             pct = static_cast<int>(std::min<int64_t>(100, (100 * need + R.smem_per_sm - 1) / R.smem_per_sm));
         }
@@ -488,17 +596,16 @@ void Runtime::launch() {
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-        const bool spec = R.spec_ok && R.specialize && !R.collect && !R.W.probe;
         if (spec)
-            (R.step_stats ? k_simulate<true, true, true> : k_simulate<true, false, true>)<<<grid, kBlock, bytes, R.stream>>>(
-                R.W, nullptr, nullptr, R.smem_heap);
+            (R.step_stats ? k_simulate<true, true, true> : k_simulate<true, false, true>)<<<sgrid, kBlock, bytes, R.stream>>>(
+                R.W, plist, pcount, R.smem_heap);
         else if (R.W.c.awc)
-            (R.step_stats ? k_simulate<true, true, false, true> : k_simulate<true, false, false, true>)<<<grid, kBlock, bytes,
+            (R.step_stats ? k_simulate<true, true, false, true> : k_simulate<true, false, false, true>)<<<sgrid, kBlock, bytes,
                                                                                                     R.stream>>>(
-                R.W, nullptr, nullptr, R.smem_heap);
+                R.W, plist, pcount, R.smem_heap);
         else
-            (R.step_stats ? k_simulate<true, true> : k_simulate<true, false>)<<<grid, kBlock, bytes, R.stream>>>(
-                R.W, nullptr, nullptr, R.smem_heap);
+            (R.step_stats ? k_simulate<true, true> : k_simulate<true, false>)<<<sgrid, kBlock, bytes, R.stream>>>(
+                R.W, plist, pcount, R.smem_heap);
         DSD_CUDA(cudaGetLastError());
         // replicas whose event heap outgrew shared memory run again from HBM
         R.ovf.ensure(4 * (R.n + 1));

@@ -130,19 +130,22 @@ def test_specialized_kernel_matches_generic_and_reference(smem_heap):
             "  workload.acceptance_rate: [0.5, 0.9]\n  workload.rate_rps: [2, 40]\n")
     js, _ = ref.run_sweep(spec, CFG, 4)
     sums = {}
-    for specialize in ("1", "0"):
+    # (specialised kernel, cost-aware lane placement) on / off: the placement
+    # only chooses which thread runs which replica
+    for specialize, placement in (("1", "1"), ("0", "1"), ("1", "0")):
         os.environ["DSD_SPECIALIZE"] = specialize
+        os.environ["DSD_PLACEMENT"] = placement
         os.environ["DSD_SMEM_HEAP"] = smem_heap
         try:
             with Simulator(0) as s:
                 s.prepare_sweep(spec, base_dir=CFG)
                 s.launch()
                 s.sync()
-                sums[specialize] = s.summaries()
+                sums[specialize + placement] = s.summaries()
                 assert s.run_sweep(spec, base_dir=CFG).summary_json == js
         finally:
-            del os.environ["DSD_SPECIALIZE"]
-            del os.environ["DSD_SMEM_HEAP"]
-    assert len(sums["1"]) == 32 * 3
-    assert (sums["1"]["status"] == 0).all()
-    assert sums["1"].tobytes() == sums["0"].tobytes()
+            for k in ("DSD_SPECIALIZE", "DSD_PLACEMENT", "DSD_SMEM_HEAP"):
+                del os.environ[k]
+    assert len(sums["11"]) == 32 * 3
+    assert (sums["11"]["status"] == 0).all()
+    assert sums["11"].tobytes() == sums["01"].tobytes() == sums["10"].tobytes()
