@@ -1467,8 +1467,16 @@ struct Engine {
 // engine's poisson re-sampling (engine.cpp:224-238).  One thread per replica;
 // writes each request's complete initial record.
 // ---------------------------------------------------------------------------
-DSD_HD void init_record(ReqRec& r, int64_t arrival, int32_t prompt, int32_t output, int32_t drafter,
+DSD_HD void init_record(ReqRec& out, int64_t arrival, int32_t prompt, int32_t output, int32_t drafter,
                         int32_t bitoff, int32_t nbits, int32_t seqoff) {
+    // built in registers and written as eight 16-byte stores (records are
+    // 128-byte aligned in HBM): each of a warp's lanes writes its own
+    // replica's record, so per-field stores would cost a line per field
+    union alignas(16) Staged {
+        ReqRec r;
+        uint4 v[sizeof(ReqRec) / 16];
+    } u;
+    ReqRec& r = u.r;
     r.arrival = arrival;
     r.first = -1;
     r.done = -1;
@@ -1499,6 +1507,9 @@ DSD_HD void init_record(ReqRec& r, int64_t arrival, int32_t prompt, int32_t outp
     r.op[0] = 0;
     r.op[1] = 0;
     r.pad = 0;
+    uint4* dst = reinterpret_cast<uint4*>(&out);
+#pragma unroll
+    for (int k = 0; k < static_cast<int>(sizeof(ReqRec) / 16); ++k) dst[k] = u.v[k];
 }
 
 DSD_HD void stage_workload(const Workspace& W, int64_t rep) {
