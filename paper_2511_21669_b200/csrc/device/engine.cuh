@@ -1527,7 +1527,11 @@ DSD_HD void stage_workload(const Workspace& W, int64_t rep) {
         lengths.seed(gseed, kLabelLengths);
         drafter.seed(gseed, kLabelDrafter);
         double clock_ms = 0.0;
-        const double alpha = S.alpha;
+        // bernoulli(alpha) = next_unit() < alpha (rng.cpp:64-66), with
+        // next_unit() = (x >> 11) * 2^-53 exact: it holds iff the 53-bit
+        // integer (x >> 11) < ceil(alpha * 2^53) (also exact), so each draw
+        // is an integer compare instead of a conversion and a multiply
+        const uint64_t accept_below = static_cast<uint64_t>(ceil(S.alpha * 0x1.0p53));
         for (int64_t n = 0; n < S.n_requests; ++n) {
             clock_ms += arrivals.exponential(S.mean_gap_ms);
             const int64_t arr = llround(clock_ms * 1000.0);
@@ -1542,8 +1546,8 @@ DSD_HD void stage_workload(const Workspace& W, int64_t rep) {
             for (int64_t k = 0; k < o; k += 64) {
                 int64_t m = o - k < 64 ? o - k : 64;
                 uint64_t acc = 0;
-                for (int64_t j = 0; j < m; ++j) {
-                    uint64_t b = bitrng.unit() < alpha ? 1u : 0u;  // bernoulli (rng.cpp:64-66)
+                for (int j = 0; j < static_cast<int>(m); ++j) {
+                    const uint64_t b = (bitrng.next() >> 11) < accept_below ? 1u : 0u;
                     acc |= b << j;
                 }
                 bits[word++] = acc;
