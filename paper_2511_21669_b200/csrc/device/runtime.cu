@@ -541,8 +541,17 @@ void Runtime::launch() {
         return;
     }
     const unsigned grid = static_cast<unsigned>((R.n + kBlock - 1) / kBlock);
-    // the HBM variant's only shared memory: the cooperative AWC scratch
+    // the HBM variant's only shared memory: the cooperative AWC scratch; its
+    // carveout keeps just that (the rest of the array is L1, which holds the
+    // AWC weights and the replicas' state)
     const size_t hbm_smem = R.W.c.awc ? (kBlock / kLanes) * sizeof(AwcWarpScratch) : 0;
+    if (R.carveout < 0) {
+        const int64_t per_sm = std::min<int64_t>(DSD_MIN_BLOCKS, (grid + R.sms - 1) / R.sms);
+        const int64_t need = hbm_smem ? per_sm * (static_cast<int64_t>(hbm_smem) + 1024) : 0;
+        const int pct = static_cast<int>(std::min<int64_t>(100, (100 * need + R.smem_per_sm - 1) / R.smem_per_sm));
+        DSD_CUDA(cudaFuncSetAttribute(k_simulate<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        DSD_CUDA(cudaFuncSetAttribute(k_simulate<false, false, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    }
     DSD_CUDA(cudaEventRecord(R.ev[0], R.stream));
     k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, R.collect ? static_cast<int64_t*>(R.ltot.p) : nullptr, nullptr,
                                            nullptr);
