@@ -114,6 +114,33 @@ DSD_HD double avx2_dot(const double* row, const double* x, int cols) {
     return s;
 }
 
+// avx2_dot for a compile-time width: fully unrolled, so the row's weight
+// loads (read-only path) are scheduled ahead of the four add chains; the same
+// operations in the same order
+template <int C>
+DSD_HD double avx2_dot_fixed(const double* row, const double* x) {
+#ifdef __CUDA_ARCH__
+#define DSD_LDW(p) __ldg(p)
+#else
+#define DSD_LDW(p) (*(p))
+#endif
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int c = 0; c < (C & ~3); c += 4) {
+        a0 = a0 + DSD_LDW(row + c) * x[c];
+        a1 = a1 + DSD_LDW(row + c + 1) * x[c + 1];
+        a2 = a2 + DSD_LDW(row + c + 2) * x[c + 2];
+        a3 = a3 + DSD_LDW(row + c + 3) * x[c + 3];
+    }
+    double s = (a0 + a2) + (a1 + a3);
+#pragma unroll
+    for (int c = C & ~3; c < C; ++c) s += DSD_LDW(row + c) * x[c];
+    return s;
+#undef DSD_LDW
+}
+// the WC-DNN shape the reference trains (TrainHyper: 5 features, 64 hidden)
+constexpr int kAwcH = 64, kAwcI = 5;
+
 DSD_HD void matvec_avx2_order(const double* w, const double* x, const double* bias, double* y,
                               int rows, int cols) {
     for (int r = 0; r < rows; ++r) y[r] = bias[r] + avx2_dot(w + static_cast<int64_t>(r) * cols, x, cols);
@@ -151,6 +178,41 @@ __device__ __noinline__ double awc_forward_warp(const char* blob, const DevScena
     const int lane = threadIdx.x & (kLanes - 1);
     const int H = S->awc_hidden, I = S->awc_input;
     const double* p = blob_ptr<double>(blob, S->o_awc_params);
+    if (H == kAwcH && I == kAwcI) {  // compile-time widths (the trained shape)
+        constexpr int FH = kAwcH, FI = kAwcI;
+        for (int r = lane; r < FH; r += kLanes) sc->hv[r] = p[FH * FI + r] + avx2_dot_fixed<FI>(p + r * FI, x);
+        __syncwarp();
+        int64_t off = FH * FI + FH;
+        for (int b = 0; b < S->awc_blocks; ++b) {
+            const double* w1 = p + off;
+            const double* b1 = w1 + FH * FH;
+            const double* w2 = b1 + FH;
+            const double* b2 = w2 + FH * FH;
+#pragma unroll
+            for (int k = 0; k < FH / kLanes; ++k) {
+                const int r = lane + k * kLanes;
+                const double u = b1[r] + avx2_dot_fixed<FH>(w1 + r * FH, sc->hv);
+                const double sg = 1.0 / (1.0 + exp(-u));
+                sc->sv[r] = u * sg;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < FH / kLanes; ++k) {
+                const int r = lane + k * kLanes;
+                sc->hv[r] += b2[r] + avx2_dot_fixed<FH>(w2 + r * FH, sc->sv);
+            }
+            __syncwarp();
+            off += 2 * FH * FH + 2 * FH;
+        }
+        double out = 0.0;
+        if (lane == 0) {
+            const double* w_out = p + off;
+            out = w_out[FH];
+            for (int i = 0; i < FH; ++i) out += w_out[i] * sc->hv[i];
+        }
+        __syncwarp();
+        return __shfl_sync(0xffffffffu, out, 0);
+    }
     for (int r = lane; r < H; r += kLanes) sc->hv[r] = p[H * I + r] + avx2_dot(p + static_cast<int64_t>(r) * I, x, I);
     __syncwarp();
     int64_t off = static_cast<int64_t>(H) * I + H;
@@ -222,6 +284,29 @@ DSD_HD double awc_predict(const char* blob, const DevScenario& S, const double r
 DSD_HD_NOINLINE double awc_forward_lane(const char* blob, const DevScenario& S, const double* x) {
     const int H = S.awc_hidden, I = S.awc_input;
     const double* p = blob_ptr<double>(blob, S.o_awc_params);
+    if (H == kAwcH && I == kAwcI) {  // compile-time widths (the trained shape)
+        constexpr int FH = kAwcH, FI = kAwcI;
+        double h[FH], s[FH];
+        for (int r = 0; r < FH; ++r) h[r] = p[FH * FI + r] + avx2_dot_fixed<FI>(p + r * FI, x);
+        int64_t off = FH * FI + FH;
+        for (int b = 0; b < S.awc_blocks; ++b) {
+            const double* w1 = p + off;
+            const double* b1 = w1 + FH * FH;
+            const double* w2 = b1 + FH;
+            const double* b2 = w2 + FH * FH;
+            for (int r = 0; r < FH; ++r) {
+                const double u = b1[r] + avx2_dot_fixed<FH>(w1 + r * FH, h);
+                const double sg = 1.0 / (1.0 + exp(-u));  // kernels::silu (kernels_scalar.cpp:65-70)
+                s[r] = u * sg;
+            }
+            for (int r = 0; r < FH; ++r) h[r] += b2[r] + avx2_dot_fixed<FH>(w2 + r * FH, s);
+            off += 2 * FH * FH + 2 * FH;
+        }
+        const double* w_out = p + off;
+        double out = w_out[FH];
+        for (int i = 0; i < FH; ++i) out += w_out[i] * h[i];
+        return out;
+    }
     double h[kMaxHidden], u[kMaxHidden], s[kMaxHidden];
     int64_t off = 0;
     matvec_avx2_order(p + off, x, p + off + H * I, h, H, I);
