@@ -381,11 +381,17 @@ static std::vector<int32_t> placement_list(const Packed& P, size_t n, int64_t wa
         const double tau = a < 1.0 ? (1.0 - std::pow(a, g + 1.0)) / (1.0 - a) : g + 1.0;
         est[k] = static_cast<double>(d.n_requests) * (4.0 + 5.0 * std::exp(d.o_mu) / tau);
     }
+    // replicas by decreasing estimate: sort the scenarios, then a counting
+    // sort of the replicas by their scenario's rank (replica order within one)
+    const size_t ns = P.scen.size();
+    std::vector<int32_t> sorder(ns), srank(ns), start(ns + 1, 0);
+    std::iota(sorder.begin(), sorder.end(), 0);
+    std::stable_sort(sorder.begin(), sorder.end(), [&](int32_t x, int32_t y) { return est[x] > est[y]; });
+    for (size_t i = 0; i < ns; ++i) srank[static_cast<size_t>(sorder[i])] = static_cast<int32_t>(i);
+    for (size_t r = 0; r < n; ++r) ++start[static_cast<size_t>(srank[P.rep_scen[r]]) + 1];
+    for (size_t i = 0; i < ns; ++i) start[i + 1] += start[i];
     std::vector<int32_t> order(n);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
-        return est[P.rep_scen[static_cast<size_t>(x)]] > est[P.rep_scen[static_cast<size_t>(y)]];
-    });
+    for (size_t r = 0; r < n; ++r) order[static_cast<size_t>(start[static_cast<size_t>(srank[P.rep_scen[r]])]++)] = static_cast<int32_t>(r);
     const double top = est[P.rep_scen[static_cast<size_t>(order[0])]];
     if (!(top > 1.05 * est[P.rep_scen[static_cast<size_t>(order[n - 1])]])) return {};
     // tiers: >= 85% of the heaviest -> 8 lanes, >= 70% -> 16 lanes, rest 32;

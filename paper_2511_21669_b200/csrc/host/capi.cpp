@@ -3,9 +3,11 @@
 // exception crosses the ABI.
 #include <cstdlib>
 #include <cstring>
+#include <iterator>
 #include <memory>
 #include <string>
 #include <thread>
+#include <vector>
 
 #include "../device/runtime.hpp"
 #include "dsdsim.h"
@@ -18,6 +20,11 @@ struct dsd_handle {
     std::unique_ptr<dsd::Runtime> rt;
     dsd::host::Caches caches;
     std::unique_ptr<dsd::host::SweepBatch> prepared_sweep;
+    // frees the last dsd_run_sweep's host batch off the caller's path
+    std::thread reaper;
+    ~dsd_handle() {
+        if (reaper.joinable()) reaper.join();
+    }
 };
 
 namespace {
@@ -199,21 +206,32 @@ int dsd_run_sweep(dsd_handle* h, const char* sweep_yaml, const char* base_dir, c
         need(h);
         dsd::host::PhaseTimer tm("dsd_run_sweep");
         dsd::cfg::Node node = dsd::cfg::parse(sweep_yaml ? sweep_yaml : "");
+        const std::string bdir = base_dir ? base_dir : ".";
+        const std::string odir = out_dir ? out_dir : "";
+        dsd::host::SweepSpec spec = dsd::host::SweepSpec::from_node(node, bdir);
         tm.lap("parse");
-        dsd::host::SweepBatch b = dsd::host::plan_sweep(node, base_dir ? base_dir : ".", 0, 1, &h->caches);
-        tm.lap("plan");
         dsd::host::SummaryParts parts;
         const bool text = summary_json || summary_csv;
-        dsd::host::SweepTotals t = dsd::host::run_sweep(*h->rt, b, out_dir ? out_dir : "", text ? &parts : nullptr);
+        auto b = std::make_unique<dsd::host::SweepBatch>(dsd::host::plan_range(spec, 0, spec.point_count(), &h->caches));
+        tm.lap("plan");
+        const dsd::host::SweepTotals t = dsd::host::run_sweep(*h->rt, *b, odir, text ? &parts : nullptr);
         tm.lap("run");
-        // the two summary texts are independent: build the CSV alongside the JSON
-        std::string csv;
-        std::thread csv_thread;
-        if (summary_csv) csv_thread = std::thread([&] { csv = dsd::host::assemble_summary_csv(parts, b.points); });
-        if (summary_json) *summary_json = dup(dsd::host::assemble_summary_json(parts, b.points));
-        if (csv_thread.joinable()) csv_thread.join();
-        if (summary_csv) *summary_csv = dup(csv);
+        if (text) {
+            std::string js, cs;
+            dsd::host::assemble_summaries(parts, b->points, summary_json ? &js : nullptr,
+                                          summary_csv ? &cs : nullptr);
+            if (summary_json) *summary_json = dup(js);
+            if (summary_csv) *summary_csv = dup(cs);
+        }
         tm.lap("summary");
+        // tens of thousands of small host objects: release them on a helper
+        // thread (joined by the next call or dsd_destroy)
+        if (h->reaper.joinable()) h->reaper.join();
+        h->reaper = std::thread([bb = std::move(b),
+                                 pp = std::make_unique<dsd::host::SummaryParts>(std::move(parts))]() mutable {
+            bb.reset();
+            pp.reset();
+        });
         if (totals) {
             totals[0] = t.points;
             totals[1] = t.replicas;

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <filesystem>
 #include <fstream>
+#include <iterator>
 #include <cstdlib>
 #include <thread>
 
@@ -106,11 +107,36 @@ std::string point_digest(const SweepSpec& spec, size_t idx) {
     return cfg::hex16(cfg::fnv1a64(point_config(spec, idx).canonical()));
 }
 
-SweepBatch plan_sweep(const Node& node, const std::string& base_dir, int shard, int n_shards, Caches* caches) {
-    SweepBatch b;
-    b.spec = SweepSpec::from_node(node, base_dir);
+// Host threads for the per-point loops (DSD_HOST_THREADS overrides).
+static unsigned host_threads() {
+    unsigned t = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32u));
+    if (const char* e = std::getenv("DSD_HOST_THREADS")) t = static_cast<unsigned>(std::max(1, std::atoi(e)));
+    return t;
+}
+
+// fn(begin, end) over contiguous chunks of [0, n), at least `grain` items per
+// thread; the calling thread takes the first chunk.
+template <class F>
+static void parallel_chunks(size_t n, size_t grain, F&& fn) {
+    const size_t t = std::min<size_t>(host_threads(), std::max<size_t>(1, n / std::max<size_t>(grain, 1)));
+    if (t <= 1) {
+        fn(size_t{0}, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    pool.reserve(t - 1);
+    for (size_t i = 1; i < t; ++i) pool.emplace_back([&fn, n, t, i] { fn(n * i / t, n * (i + 1) / t); });
+    fn(size_t{0}, n / t);
+    for (auto& th : pool) th.join();
+}
+
+// Points [lo, hi) of b.spec (local index i = point lo + i) resolved into
+// scenarios and the replicas of one shard.
+static void plan_points(SweepBatch& b, size_t lo, size_t hi, int shard, int n_shards, Caches* caches) {
+    PhaseTimer tm("plan_sweep");
     const SweepSpec& spec = b.spec;
-    const size_t n_points = spec.point_count();
+    const size_t n_points = hi - lo;
+    b.point_base = lo;
     b.points.resize(n_points);
     // every point is materialised and resolved once, in parallel: assignment
     // and id, the config, its scenario (the digest is only computed when
@@ -119,12 +145,12 @@ SweepBatch plan_sweep(const Node& node, const std::string& base_dir, int shard, 
     std::vector<char> ok(n_points, 0);
     std::vector<std::vector<uint64_t>> seeds(n_points);
     std::atomic<size_t> next{0};
-    auto worker = [&] {
+    auto worker = [&](size_t, size_t) {
         for (;;) {
             size_t idx = next.fetch_add(1);
             if (idx >= n_points) return;
             SweepPoint& p = b.points[idx];
-            size_t rem = idx;
+            size_t rem = lo + idx;
             auto& asg = p.assignment;
             for (size_t a = spec.axes.size(); a-- > 0;) {
                 const auto& values = spec.axes[a].second;
@@ -136,7 +162,7 @@ SweepBatch plan_sweep(const Node& node, const std::string& base_dir, int shard, 
             p.point_id = point_id_of(asg);
             point_seeds(spec.base_seed, p.point_id, spec.repetitions, seeds[idx]);
             try {
-                res[idx] = resolve_config(point_config(spec, idx), true, seeds[idx][0], spec.base_dir, caches,
+                res[idx] = resolve_config(point_config(spec, lo + idx), true, seeds[idx][0], spec.base_dir, caches,
                                           /*want_digest=*/false);
                 ok[idx] = 1;
             } catch (const std::exception& e) {
@@ -145,49 +171,59 @@ SweepBatch plan_sweep(const Node& node, const std::string& base_dir, int shard, 
             }
         }
     };
-    unsigned nthreads = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32u));
-    if (const char* e = std::getenv("DSD_HOST_THREADS")) nthreads = std::max(1, std::atoi(e));
-    if (n_points < 64) nthreads = 1;
-    if (nthreads == 1) {
-        worker();
-    } else {
-        std::vector<std::thread> pool;
-        for (unsigned t = 0; t < nthreads; ++t) pool.emplace_back(worker);
-        for (auto& t : pool) t.join();
-    }
+    // one work-stealing worker per thread (points differ in cost)
+    parallel_chunks(n_points < 64 ? 1 : std::min<size_t>(n_points, host_threads()), 1, worker);
+    tm.lap("points");
+    // resolved scenarios in point order, then the replicas of this shard:
+    // global replica g = scenario * repetitions + rep, kept when g % n_shards
+    // == shard, at position g / n_shards
     b.point_scenario.assign(n_points, -1);
     size_t n_ok = 0;
-    for (size_t idx = 0; idx < n_points; ++idx) n_ok += ok[idx];
-    b.resolved.reserve(n_ok);
-    for (size_t idx = 0; idx < n_points; ++idx) {
-        if (!ok[idx]) continue;
-        b.point_scenario[idx] = static_cast<int64_t>(b.resolved.size());
-        b.resolved.push_back(std::move(res[idx]));
-    }
-    b.scenarios.reserve(b.resolved.size());
-    for (auto& r : b.resolved) {
-        r.bind();
-        b.scenarios.push_back(r.scen);
-    }
-    const size_t n_rep = n_ok * static_cast<size_t>(spec.repetitions);
-    const size_t mine = n_shards > 1 ? (n_rep + static_cast<size_t>(n_shards) - 1) / n_shards : n_rep;
-    b.replicas.reserve(mine);
-    b.replica_origin.reserve(mine);
-    int64_t g = 0;
-    for (size_t idx = 0; idx < n_points; ++idx) {
-        const int64_t s = b.point_scenario[idx];
-        if (s < 0) continue;
-        const Resolved& r = b.resolved[static_cast<size_t>(s)];
-        for (int rep = 0; rep < spec.repetitions; ++rep, ++g) {
-            if (n_shards > 1 && g % n_shards != shard) continue;
-            dsd_replica x{};
-            x.scenario = static_cast<uint32_t>(s);
-            x.seed = seeds[idx][static_cast<size_t>(rep)];
-            x.gen_seed = r.gen_seed_fixed ? r.gen_seed : x.seed;
-            b.replicas.push_back(x);
-            b.replica_origin.emplace_back(static_cast<int64_t>(idx), rep);
+    for (size_t idx = 0; idx < n_points; ++idx)
+        if (ok[idx]) b.point_scenario[idx] = static_cast<int64_t>(n_ok++);
+    const size_t R = static_cast<size_t>(spec.repetitions);
+    const size_t N = n_shards > 1 ? static_cast<size_t>(n_shards) : 1;
+    const size_t sh = n_shards > 1 ? static_cast<size_t>(shard) : 0;
+    const size_t n_rep = n_ok * R;
+    const size_t mine = n_rep > sh ? (n_rep - sh - 1) / N + 1 : 0;
+    b.resolved.resize(n_ok);
+    b.scenarios.resize(n_ok);
+    b.replicas.resize(mine);
+    b.replica_origin.resize(mine);
+    parallel_chunks(n_points, 256, [&](size_t lo, size_t hi) {
+        for (size_t idx = lo; idx < hi; ++idx) {
+            const int64_t s = b.point_scenario[idx];
+            if (s < 0) continue;
+            Resolved& r = b.resolved[static_cast<size_t>(s)];
+            r = std::move(res[idx]);
+            r.bind();
+            b.scenarios[static_cast<size_t>(s)] = r.scen;
+            for (size_t rep = 0; rep < R; ++rep) {
+                const size_t g = static_cast<size_t>(s) * R + rep;
+                if (g % N != sh) continue;
+                dsd_replica& x = b.replicas[g / N];
+                x = dsd_replica{};
+                x.scenario = static_cast<uint32_t>(s);
+                x.seed = seeds[idx][rep];
+                x.gen_seed = r.gen_seed_fixed ? r.gen_seed : x.seed;
+                b.replica_origin[g / N] = {static_cast<int64_t>(idx), static_cast<int>(rep)};
+            }
         }
-    }
+    });
+    tm.lap("replicas");
+}
+
+SweepBatch plan_sweep(const Node& node, const std::string& base_dir, int shard, int n_shards, Caches* caches) {
+    SweepBatch b;
+    b.spec = SweepSpec::from_node(node, base_dir);
+    plan_points(b, 0, b.spec.point_count(), shard, n_shards, caches);
+    return b;
+}
+
+SweepBatch plan_range(const SweepSpec& spec, size_t lo, size_t hi, Caches* caches) {
+    SweepBatch b;
+    b.spec = spec;
+    plan_points(b, lo, hi, 0, 1, caches);
     return b;
 }
 
@@ -201,20 +237,20 @@ void PhaseTimer::lap(const char* phase) {
     t_ = t;
 }
 
-SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir, SummaryParts* parts) {
-    SweepTotals tot;
+void launch_batch(Runtime& rt, SweepBatch& b, bool reports) {
+    PhaseTimer tm("run_sweep");
+    if (b.replicas.empty()) return;
+    rt.prepare(b.scenarios.data(), b.scenarios.size(), b.replicas.data(), b.replicas.size(), reports);
+    tm.lap("prepare");
+    rt.launch();
+}
+
+void collect_batch(Runtime& rt, SweepBatch& b, const std::string& out_dir, SweepTotals& tot) {
     PhaseTimer tm("run_sweep");
     const bool reports = !out_dir.empty();
-    if (reports) std::filesystem::create_directories(out_dir);
     const size_t n = b.replicas.size();
     std::vector<dsd_replica_summary> sums(n);
     if (n > 0) {
-        rt.prepare(b.scenarios.data(), b.scenarios.size(), b.replicas.data(), n, reports);
-        tm.lap("prepare");
-        rt.launch();
-        // the host is idle while the kernels run: render the summary text
-        // that does not depend on the results
-        if (parts) *parts = render_summary_prefixes(b.points);
         rt.sync();
         tm.lap("kernels");
         rt.summaries(sums.data(), n);
@@ -223,42 +259,64 @@ SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir, Su
     const int R = b.spec.repetitions;
     std::vector<double> thr(b.points.size(), 0.0), ttft(b.points.size(), 0.0), tpot(b.points.size(), 0.0);
     std::vector<std::string> digest(reports ? b.points.size() : 0);  // config digests, on first use
-    if (n == 0 && parts) *parts = render_summary_prefixes(b.points);
-    for (size_t k = 0; k < n; ++k) {  // replicas are point-major, rep-minor: sums in rep order
-        const auto [p, rep] = b.replica_origin[k];
-        SweepPoint& pt = b.points[static_cast<size_t>(p)];
-        const dsd_replica_summary& s = sums[k];
-        tot.events += static_cast<double>(s.events_processed);
-        tot.replicas += 1;
-        if (s.status != DSD_OK) {
-            pt.failed = true;
-            pt.error = "engine capacity exceeded on the device (event heap / sequence arena)";
-            continue;
+    // replicas k in [lo, hi): a point's replicas are contiguous (plan_sweep
+    // places them in (point, rep) order), so chunks that start and end on
+    // point boundaries own their points and sum them in rep order
+    auto accumulate = [&](size_t lo, size_t hi, SweepTotals& t) {
+        for (size_t k = lo; k < hi; ++k) {
+            const auto [p, rep] = b.replica_origin[k];
+            SweepPoint& pt = b.points[static_cast<size_t>(p)];
+            const dsd_replica_summary& s = sums[k];
+            t.events += static_cast<double>(s.events_processed);
+            t.replicas += 1;
+            if (s.status != DSD_OK) {
+                pt.failed = true;
+                pt.error = "engine capacity exceeded on the device (event heap / sequence arena)";
+                continue;
+            }
+            thr[p] += s.throughput_rps;
+            ttft[p] += s.mean_ttft_ms;
+            tpot[p] += s.mean_tpot_ms;
+            if (reports) {
+                const Resolved& r = b.resolved[static_cast<size_t>(b.point_scenario[p])];
+                ReplicaOutput out;
+                out.summary = s;
+                int64_t nrec = 0, nseq = 0;
+                rt.fetch_records(k, nullptr, 0, &nrec, nullptr, nullptr, 0, &nseq, nullptr, 0);
+                out.records.resize(static_cast<size_t>(nrec));
+                out.gamma_seq.resize(static_cast<size_t>(nseq));
+                out.committed_seq.resize(static_cast<size_t>(nseq));
+                out.busy_us.resize(static_cast<size_t>(r.scen.n_targets));
+                rt.fetch_records(k, out.records.data(), out.records.size(), &nrec, out.gamma_seq.data(),
+                                 out.committed_seq.data(), out.gamma_seq.size(), &nseq, out.busy_us.data(),
+                                 out.busy_us.size());
+                const std::string file =
+                    out_dir + "/" + sanitize_filename(pt.point_id) + "_rep" + std::to_string(rep) + ".json";
+                std::ofstream f(file, std::ios::binary);
+                if (!f) throw Error(DSD_ERR_RUNTIME, "cannot write file: " + file);
+                std::string& dg = digest[static_cast<size_t>(p)];
+                if (dg.empty()) dg = point_digest(b.spec, b.point_base + static_cast<size_t>(p));
+                f << emit_report(out, r.scen.n_targets, dg, b.replicas[k].seed);
+                pt.report_files.push_back(file);
+            }
         }
-        thr[p] += s.throughput_rps;
-        ttft[p] += s.mean_ttft_ms;
-        tpot[p] += s.mean_tpot_ms;
-        if (reports) {
-            const Resolved& r = b.resolved[static_cast<size_t>(b.point_scenario[p])];
-            ReplicaOutput out;
-            out.summary = s;
-            int64_t nrec = 0, nseq = 0;
-            rt.fetch_records(k, nullptr, 0, &nrec, nullptr, nullptr, 0, &nseq, nullptr, 0);
-            out.records.resize(static_cast<size_t>(nrec));
-            out.gamma_seq.resize(static_cast<size_t>(nseq));
-            out.committed_seq.resize(static_cast<size_t>(nseq));
-            out.busy_us.resize(static_cast<size_t>(r.scen.n_targets));
-            rt.fetch_records(k, out.records.data(), out.records.size(), &nrec, out.gamma_seq.data(),
-                             out.committed_seq.data(), out.gamma_seq.size(), &nseq, out.busy_us.data(),
-                             out.busy_us.size());
-            const std::string file =
-                out_dir + "/" + sanitize_filename(pt.point_id) + "_rep" + std::to_string(rep) + ".json";
-            std::ofstream f(file, std::ios::binary);
-            if (!f) throw Error(DSD_ERR_RUNTIME, "cannot write file: " + file);
-            std::string& dg = digest[static_cast<size_t>(p)];
-            if (dg.empty()) dg = point_digest(b.spec, static_cast<size_t>(p));
-            f << emit_report(out, r.scen.n_targets, dg, b.replicas[k].seed);
-            pt.report_files.push_back(file);
+    };
+    if (reports || n < 4096) {
+        accumulate(0, n, tot);
+    } else {
+        std::vector<SweepTotals> part(host_threads());
+        std::atomic<size_t> slot{0};
+        parallel_chunks(n, 2048, [&](size_t lo, size_t hi) {
+            auto boundary = [&](size_t k) {
+                while (k > 0 && k < n && b.replica_origin[k].first == b.replica_origin[k - 1].first) ++k;
+                return k;
+            };
+            SweepTotals& t = part[slot.fetch_add(1)];
+            accumulate(boundary(lo), boundary(hi), t);
+        });
+        for (const SweepTotals& t : part) {  // integer-valued totals: any order is exact
+            tot.events += t.events;
+            tot.replicas += t.replicas;
         }
     }
     tm.lap(reports ? "reports" : "aggregate");
@@ -273,6 +331,17 @@ SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir, Su
         pt.mean_ttft_ms = ttft[p] / R;
         pt.mean_tpot_ms = tpot[p] / R;
     }
+}
+
+SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir, SummaryParts* parts) {
+    SweepTotals tot;
+    const bool reports = !out_dir.empty();
+    if (reports) std::filesystem::create_directories(out_dir);
+    launch_batch(rt, b, reports);
+    // the host is idle while the kernels run: render the summary text that
+    // does not depend on the results
+    if (parts) *parts = render_summary_prefixes(b.points, b.point_base);
+    collect_batch(rt, b, out_dir, tot);
     return tot;
 }
 
@@ -280,14 +349,14 @@ SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir, Su
 // JsonOut writes (2-space indent), split per point into the part that is
 // known before the simulation (id, assignment) and the part that needs its
 // results, so run_sweep renders the former while the kernels run.
-SummaryParts render_summary_prefixes(const std::vector<SweepPoint>& points) {
+SummaryParts render_summary_prefixes(const std::vector<SweepPoint>& points, size_t first) {
     SummaryParts parts;
     parts.json.resize(points.size());
     parts.csv.resize(points.size());
     for (size_t i = 0; i < points.size(); ++i) {
         const SweepPoint& p = points[i];
         std::string& j = parts.json[i];
-        j += i ? ",\n    {\n      \"point\": \"" : "\n    {\n      \"point\": \"";
+        j += first + i ? ",\n    {\n      \"point\": \"" : "\n    {\n      \"point\": \"";
         cfg::json_escape(j, p.point_id);
         j += "\",\n      \"assignment\": {";
         for (size_t k = 0; k < p.assignment.size(); ++k) {
@@ -304,42 +373,81 @@ SummaryParts render_summary_prefixes(const std::vector<SweepPoint>& points) {
     return parts;
 }
 
-std::string assemble_summary_json(const SummaryParts& parts, const std::vector<SweepPoint>& points) {
-    std::string out = "{\n  \"points\": [";
-    for (size_t i = 0; i < points.size(); ++i) {
-        const SweepPoint& p = points[i];
-        out += parts.json[i];
+// The point's entry after its prefix; json and/or csv may be null.
+static void render_point(const SummaryParts& parts, const SweepPoint& p, size_t i, std::string* j, std::string* c) {
+    std::string thr, ttft, tpot;
+    if (c || !p.failed) {
+        thr = cfg::fmt_fixed(p.mean_throughput_rps, 6);
+        ttft = cfg::fmt_fixed(p.mean_ttft_ms, 3);
+        tpot = cfg::fmt_fixed(p.mean_tpot_ms, 3);
+    }
+    if (j) {
+        *j += parts.json[i];
         if (p.failed) {
-            out += "true,\n      \"error\": \"";
-            cfg::json_escape(out, p.error);
-            out += "\"\n    }";
+            *j += "true,\n      \"error\": \"";
+            cfg::json_escape(*j, p.error);
+            *j += "\"\n    }";
         } else {
-            out += "false,\n      \"throughput_rps\": ";
-            out += cfg::fmt_fixed(p.mean_throughput_rps, 6);
-            out += ",\n      \"mean_ttft_ms\": ";
-            out += cfg::fmt_fixed(p.mean_ttft_ms, 3);
-            out += ",\n      \"mean_tpot_ms\": ";
-            out += cfg::fmt_fixed(p.mean_tpot_ms, 3);
-            out += "\n    }";
+            *j += "false,\n      \"throughput_rps\": ";
+            *j += thr;
+            *j += ",\n      \"mean_ttft_ms\": ";
+            *j += ttft;
+            *j += ",\n      \"mean_tpot_ms\": ";
+            *j += tpot;
+            *j += "\n    }";
         }
     }
-    out += points.empty() ? "]\n}\n" : "\n  ]\n}\n";
+    if (c) {
+        *c += parts.csv[i];
+        *c += p.failed ? "1," : "0,";
+        *c += thr;
+        *c += ',';
+        *c += ttft;
+        *c += ',';
+        *c += tpot;
+        *c += '\n';
+    }
+}
+
+void assemble_summaries(const SummaryParts& parts, const std::vector<SweepPoint>& points, std::string* json,
+                        std::string* csv) {
+    const size_t n = points.size();
+    // contiguous point ranges rendered in parallel, then concatenated
+    const size_t chunks = std::max<size_t>(1, std::min<size_t>(host_threads(), n / 512));
+    std::vector<std::string> cj(chunks), cc(chunks);
+    parallel_chunks(chunks, 1, [&](size_t c0, size_t c1) {
+        for (size_t c = c0; c < c1; ++c)
+            for (size_t i = n * c / chunks; i < n * (c + 1) / chunks; ++i)
+                render_point(parts, points[i], i, json ? &cj[c] : nullptr, csv ? &cc[c] : nullptr);
+    });
+    if (json) {
+        size_t len = 32;
+        for (const auto& x : cj) len += x.size();
+        json->clear();
+        json->reserve(len);
+        *json += "{\n  \"points\": [";
+        for (const auto& x : cj) *json += x;
+        *json += points.empty() ? "]\n}\n" : "\n  ]\n}\n";
+    }
+    if (csv) {
+        size_t len = 64;
+        for (const auto& x : cc) len += x.size();
+        csv->clear();
+        csv->reserve(len);
+        *csv += "point,failed,throughput_rps,mean_ttft_ms,mean_tpot_ms\n";
+        for (const auto& x : cc) *csv += x;
+    }
+}
+
+std::string assemble_summary_json(const SummaryParts& parts, const std::vector<SweepPoint>& points) {
+    std::string out;
+    assemble_summaries(parts, points, &out, nullptr);
     return out;
 }
 
 std::string assemble_summary_csv(const SummaryParts& parts, const std::vector<SweepPoint>& points) {
-    std::string out = "point,failed,throughput_rps,mean_ttft_ms,mean_tpot_ms\n";
-    for (size_t i = 0; i < points.size(); ++i) {
-        const SweepPoint& p = points[i];
-        out += parts.csv[i];
-        out += p.failed ? "1," : "0,";
-        out += cfg::fmt_fixed(p.mean_throughput_rps, 6);
-        out += ',';
-        out += cfg::fmt_fixed(p.mean_ttft_ms, 3);
-        out += ',';
-        out += cfg::fmt_fixed(p.mean_tpot_ms, 3);
-        out += '\n';
-    }
+    std::string out;
+    assemble_summaries(parts, points, nullptr, &out);
     return out;
 }
 

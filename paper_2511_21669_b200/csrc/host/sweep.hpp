@@ -45,9 +45,12 @@ struct SweepBatch {
     std::vector<dsd_scenario> scenarios;
     std::vector<dsd_replica> replicas;
     std::vector<std::pair<int64_t, int>> replica_origin;  // replica -> (point, rep)
+    size_t point_base = 0;  // points[i] is sweep point point_base + i
 };
 
 SweepBatch plan_sweep(const cfg::Node& node, const std::string& base_dir, int shard, int n_shards, Caches* caches);
+// Points [lo, hi) of a parsed spec, every replica (no sharding).
+SweepBatch plan_range(const SweepSpec& spec, size_t lo, size_t hi, Caches* caches);
 
 // DSD_HOST_TIMING=1: phase durations of the host sweep path to stderr
 class PhaseTimer {
@@ -70,13 +73,21 @@ struct SweepTotals {
 struct SummaryParts {
     std::vector<std::string> json, csv;
 };
-SummaryParts render_summary_prefixes(const std::vector<SweepPoint>& points);
+// `first`: the sweep index of points[0] (the separator before the first entry)
+SummaryParts render_summary_prefixes(const std::vector<SweepPoint>& points, size_t first = 0);
+// Both texts in one parallel pass (either may be null).
+void assemble_summaries(const SummaryParts& parts, const std::vector<SweepPoint>& points, std::string* json,
+                        std::string* csv);
 std::string assemble_summary_json(const SummaryParts& parts, const std::vector<SweepPoint>& points);
 std::string assemble_summary_csv(const SummaryParts& parts, const std::vector<SweepPoint>& points);
 
 // run_sweep on the GPU; writes per-replica reports when out_dir is non-empty.
 // With `parts`, the summary prefixes are rendered while the kernels run.
 SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir, SummaryParts* parts = nullptr);
+// The two halves of run_sweep: enqueue the batch on rt; wait for it and fill
+// the points' means (writing reports when out_dir is set) into `tot`.
+void launch_batch(Runtime& rt, SweepBatch& b, bool reports);
+void collect_batch(Runtime& rt, SweepBatch& b, const std::string& out_dir, SweepTotals& tot);
 std::string sweep_summary_json(const std::vector<SweepPoint>& points);
 std::string sweep_summary_csv(const std::vector<SweepPoint>& points);
 
