@@ -100,6 +100,31 @@ def test_sweep_report_files_match_reference(sim, tmp_path):
         assert (ref_dir / f).read_bytes() == (my_dir / f).read_bytes(), f
 
 
+def test_large_sweep_parallel_aggregation_matches_reference():
+    """A sweep above the host's parallel thresholds (4,096 replicas for the
+    per-point sums, 1,024 points for the summary text): sums split across host
+    threads at point boundaries (7 repetitions, so the raw split falls inside a
+    point), failed points (max_batch_size 0) among them; the summaries must
+    equal the reference's with any host thread count."""
+    from paper_2511_21669_b200 import Simulator
+    spec = ("base: c1_single_pair.yaml\nseed: 5\nrepetitions: 7\naxes:\n"
+            "  policies.window.gamma: [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16]\n"
+            "  network.rtt_ms: [2, 6, 10, 14, 20, 30, 45, 60]\n"
+            "  policies.batching.max_batch_size: [0, 4, 8, 16]\n"
+            "  workload.acceptance_rate: [0.6, 0.9]\n  workload.n_requests: [30]\n")
+    js, cs = ref.run_sweep(spec, CFG, 8)
+    for threads in ("16", "1"):
+        os.environ["DSD_HOST_THREADS"] = threads
+        try:
+            with Simulator(0) as s:
+                out = s.run_sweep(spec, base_dir=CFG)
+        finally:
+            del os.environ["DSD_HOST_THREADS"]
+        assert (out.points, out.replicas, out.failed_points) == (1024, 768 * 7, 256)
+        assert out.summary_json == js
+        assert out.summary_csv == cs
+
+
 @pytest.mark.parametrize("smem_heap", ["0", "2", "8"])
 def test_kernel_variants_and_overflow_rerun(smem_heap):
     """HBM variant (0), shared-memory variant with forced heap overflow and
