@@ -21,7 +21,12 @@ namespace {
 struct BlobBuilder {
     std::vector<char> data;
     std::unordered_map<const void*, int64_t> seen;
+    // Arrays shared between scenarios (latency grids, traces, AWC weights)
+    // are stored once, keyed by their host address; a scenario's own small
+    // arrays (groups, grid indices) are simply appended.
+    static constexpr size_t kDedupeMin = 256;
     int64_t put(const void* src, size_t bytes, bool dedupe = true) {
+        dedupe = dedupe && bytes >= kDedupeMin;
         if (dedupe && src) {
             auto it = seen.find(src);
             if (it != seen.end()) return it->second;
@@ -72,12 +77,20 @@ int64_t axis_table(BlobBuilder& B, const double* axis, int n, int32_t* size) {
 }  // namespace
 
 Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n, bool probe) {
-    if (ns == 0 && n > 0) cfg_error("batch has replicas but no scenarios");
     Packed P;
+    pack_batch_into(P, sc, ns, reps, n, probe);
+    return P;
+}
+
+void pack_batch_into(Packed& P, const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n, bool probe) {
+    if (ns == 0 && n > 0) cfg_error("batch has replicas but no scenarios");
     BlobBuilder B;
+    B.data = std::move(P.blob);
+    B.data.clear();
     B.data.reserve(256 * ns + (1u << 16));
-    B.seen.reserve(8 * ns);
+    B.seen.reserve(64);
     std::vector<DevScenario>& ds = P.scen;
+    ds.clear();
     ds.resize(ns);
     Caps& c = P.caps;
     c = Caps{};
@@ -341,7 +354,6 @@ Packed pack_batch(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, si
     c.nwarps = (c.n + kLanes - 1) / kLanes;
 
     P.blob = std::move(B.data);
-    return P;
 }
 
 size_t layout_workspace(Workspace& W, const Caps& c, char* base) {

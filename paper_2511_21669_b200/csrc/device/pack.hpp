@@ -23,6 +23,10 @@ struct Packed {
 // keeps the pair metric rings (the reference always does).
 Packed pack_batch(const dsd_scenario* scenarios, size_t n_scenarios, const dsd_replica* replicas, size_t n,
                   bool probe = false);
+// The same into P, reusing its vectors' storage (a Runtime packs every batch
+// into one Packed, so repeated batches touch no fresh host pages).
+void pack_batch_into(Packed& P, const dsd_scenario* scenarios, size_t n_scenarios, const dsd_replica* replicas,
+                     size_t n, bool probe);
 
 // Assigns the workspace field pointers inside [base, base + bytes) and
 // returns bytes; with base == nullptr it only sizes.

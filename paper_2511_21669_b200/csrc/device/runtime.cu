@@ -296,7 +296,7 @@ struct RuntimeImpl {
     int sms = 148, smem_per_sm = 228 * 1024;
     DevBuf stats;
     Workspace W{};
-    std::vector<DevScenario> host_scen;
+    Packed packed;  // the last batch, host side (storage reused across batches)
     std::vector<int64_t> host_seqbase;
     std::vector<int64_t> host_ltot;
     size_t n = 0;
@@ -449,7 +449,8 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
                      std::chrono::duration<double, std::milli>(t - t_prev).count());
         t_prev = t;
     };
-    Packed P = pack_batch(sc, ns, reps, n, feature_probe);
+    Packed& P = R.packed;
+    pack_batch_into(P, sc, ns, reps, n, feature_probe);
     lap("pack");
     const Caps& c = P.caps;
     // ---- upload blob, scenarios, replicas ----
@@ -526,7 +527,6 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
         DSD_CUDA(cudaMemcpyAsync(R.place.p, pl.data(), 4 * pl.size(), cudaMemcpyHostToDevice, R.stream));
         R.place_n = nw * kLanes;
     }
-    R.host_scen = std::move(P.scen);
     R.n = n;
     R.collect = collect;
     if (collect) R.ltot.ensure(sizeof(int64_t) * std::max<size_t>(n, 1));
@@ -731,7 +731,7 @@ void Runtime::fetch_records(size_t replica, dsd_request_record* records, size_t 
         DSD_CUDA(cudaStreamSynchronize(R.stream));
         R.rec_cached = true;
     }
-    const DevScenario& S = R.host_scen[0];
+    const DevScenario& S = R.packed.scen[0];
     (void)S;
     dsd_replica_summary sm;
     DSD_CUDA(cudaMemcpy(&sm, static_cast<DevSummary*>(R.summary.p) + replica, sizeof(sm), cudaMemcpyDeviceToHost));

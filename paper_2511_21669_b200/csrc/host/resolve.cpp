@@ -509,9 +509,10 @@ std::shared_ptr<const T> cached(Caches* caches, std::map<std::string, std::share
         if (it != m.end()) return it->second;
     }
     auto v = make();
+    // planner threads that missed together share the first table inserted
+    // (one copy of each latency grid in the device blob)
     std::lock_guard<std::mutex> lk(caches->mu);
-    (caches->*slot)[key] = v;
-    return v;
+    return (caches->*slot).emplace(key, std::move(v)).first->second;
 }
 
 }  // namespace
