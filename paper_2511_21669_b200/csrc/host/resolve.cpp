@@ -16,6 +16,8 @@
 #include <cmath>
 #include <fstream>
 #include <set>
+#include <initializer_list>
+#include <string_view>
 #include <sstream>
 
 #include <json.hpp>
@@ -37,11 +39,12 @@ const char* kCloudHw = "cloud-gpu";
 const char* kDraftModel = "draft-model";
 const char* kEdgeHw = "edge-gpu";
 
-void check_keys(const Node& n, const std::set<std::string>& allowed, const std::string& where, bool strict) {
+// (a handful of literal keys: a linear scan, no per-call allocation)
+void check_keys(const Node& n, std::initializer_list<std::string_view> allowed, std::string_view where, bool strict) {
     if (!strict || !n.map()) return;
     for (const auto& f : n.fields)
-        if (!allowed.count(f.first))
-            config_error("unknown key '" + f.first + "' in " + where + " (use lenient mode to ignore)");
+        if (std::find(allowed.begin(), allowed.end(), std::string_view(f.first)) == allowed.end())
+            config_error("unknown key '" + f.first + "' in " + std::string(where) + " (use lenient mode to ignore)");
 }
 
 struct Group {
