@@ -394,8 +394,9 @@ static std::vector<int32_t> placement_list(const Packed& P, size_t n, int64_t wa
     for (size_t r = 0; r < n; ++r) order[static_cast<size_t>(start[static_cast<size_t>(srank[P.rep_scen[r]])]++)] = static_cast<int32_t>(r);
     const double top = est[P.rep_scen[static_cast<size_t>(order[0])]];
     if (!(top > 1.05 * est[P.rep_scen[static_cast<size_t>(order[n - 1])]])) return {};
-    // tiers: >= 85% of the heaviest -> 8 lanes, >= 70% -> 16 lanes, rest 32;
-    // shrink the thin tiers until the warps fit one wave
+    // tiers: >= 90% of the heaviest -> 8 lanes, >= 75% -> 16 lanes, rest 32
+    // (DSD_PLACE_T8 / DSD_PLACE_T16); shrink the thin tiers until the warps
+    // fit one wave
     static const double th8 = std::getenv("DSD_PLACE_T8") ? std::atof(std::getenv("DSD_PLACE_T8")) : 0.90;
     static const double th16 = std::getenv("DSD_PLACE_T16") ? std::atof(std::getenv("DSD_PLACE_T16")) : 0.75;
     int64_t t8 = 0, t16 = 0;
