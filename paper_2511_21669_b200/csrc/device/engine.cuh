@@ -42,6 +42,12 @@ DSD_HD const T* blob_ptr(const char* blob, int64_t off) {
     return reinterpret_cast<const T*>(blob + off);
 }
 
+#ifndef DSD_SPEC_STACK
+#define DSD_SPEC_STACK 2
+#endif
+// action-stack depth of the specialised kernel (2..4)
+constexpr int kSpecStack = DSD_SPEC_STACK;
+
 // ---------------------------------------------------------------------------
 // latency model: Grid::interpolate (profile.cpp:57-88) + predict (:129-151)
 // ---------------------------------------------------------------------------
@@ -506,6 +512,7 @@ struct Engine {
     // passes a compile-time true, so T, D and the policy flags below become
     // constants and the generic paths fold away: a smaller, faster event loop.
     bool spec;
+    int spec_limit;  // overflow limit of the specialised stack (a kernel template constant)
     static constexpr uint32_t kSpecFlags = (1u << 3) | (1u << 9);  // jitter_free | single_link
     // specialised kernel only: the four latency grids (target / draft x
     // prefill / decode-shaped) and the link's one-way delay, resolved once
@@ -517,9 +524,11 @@ struct Engine {
 
     DSD_HD Engine(const Workspace& w, const DevScenario& s, int64_t replica, int32_t* server_base,
                   int64_t* heap_time_base, uint64_t* heap_key_base, int64_t heap_cap, int32_t server_cap,
-                  unsigned char* hot_base = nullptr, bool specialized = false, AwcWarpScratch* awc_scratch = nullptr)
+                  unsigned char* hot_base = nullptr, bool specialized = false, AwcWarpScratch* awc_scratch = nullptr,
+                  int spec_stack_limit = kSpecStack)
         : W(w), S(s), rep(static_cast<int32_t>(replica)), sb(server_base), htb(heap_time_base),
-          hkb(heap_key_base), hcap(static_cast<int32_t>(heap_cap)), nsc(server_cap), spec(specialized) {
+          hkb(heap_key_base), hcap(static_cast<int32_t>(heap_cap)), nsc(server_cap), spec(specialized),
+          spec_limit(spec_stack_limit) {
         R = W.req + replica * W.c.nr;
         gamma_s = S.gamma;
         max_batch = S.max_batch;
@@ -610,13 +619,17 @@ struct Engine {
 
     // ---- action stack ----
     static DSD_HD uint32_t act(uint32_t kind, uint32_t arg) { return kind | (arg << 4); }
+    // Depth 4 (st0..st3); the specialised kernel keeps kSpecStack slots (fewer
+    // registers to shift and to merge at every join), and a replica that
+    // would need more fails with kFailStack and runs again on the HBM variant.
+    DSD_HD int stack_cap() const { return spec ? kSpecStack : 4; }
     DSD_HD void push_act(uint32_t a) {
-        if (sp >= 4) {
+        if (sp >= (spec ? spec_limit : 4)) {
             fail = kFailStack;
             return;
         }
-        st3 = st2;
-        st2 = st1;
+        if (stack_cap() > 3) st3 = st2;
+        if (stack_cap() > 2) st2 = st1;
         st1 = st0;
         st0 = a;
         ++sp;
@@ -624,8 +637,8 @@ struct Engine {
     DSD_HD uint32_t pop_act() {
         uint32_t a = st0;
         st0 = st1;
-        st1 = st2;
-        st2 = st3;
+        if (stack_cap() > 2) st1 = st2;
+        if (stack_cap() > 3) st2 = st3;
         --sp;
         return a;
     }

@@ -126,7 +126,9 @@ __device__ __forceinline__ uint32_t vote_kind(unsigned best) {
 // kSpec: the single-pair specialisation (Engine::spec; kSmem only).
 // kAwc: the batch has AWC scenarios (cooperative AWC scratch + serving); the
 // other instantiations compile that code out.
-template <bool kSmem, bool kStats, bool kSpec = false, bool kAwc = false>
+// kSpecLimit: overflow limit of the specialised action stack (1 only in the
+// test instantiation that forces the HBM re-run, DSD_SPEC_STACK_LIMIT=1).
+template <bool kSmem, bool kStats, bool kSpec = false, bool kAwc = false, int kSpecLimit = kSpecStack>
 __global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_BLOCKS) k_simulate(const __grid_constant__ Workspace W,
                                                                       const int32_t* list, const int32_t* count,
                                                      int32_t smem_heap_cap) {
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_
         if constexpr (kAwc) awc = reinterpret_cast<AwcWarpScratch*>(smem) + threadIdx.x / kLanes;
     }
     if constexpr (kAwc) awc->req[threadIdx.x % kLanes] = 0;
-    Engine e(W, W.scen[W.rep_scen[r]], r, sbase, hb, kb, hcap, nsc, hot, kSpec, awc);
+    Engine e(W, W.scen[W.rep_scen[r]], r, sbase, hb, kb, hcap, nsc, hot, kSpec, awc, kSpecLimit);
     if (live) e.init();
     uint32_t kind = live ? e.next_kind() : static_cast<uint32_t>(kActNone);
     // kStats: per-step-kind cycle profile (DSD_STEP_STATS=1), one block-level
@@ -217,11 +219,12 @@ __global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_
     if (live) e.finish();
 }
 
-// Collects the replicas whose shared-memory heap overflowed.
+// Collects the replicas whose shared-memory heap (or the specialised
+// kernel's shorter action stack) overflowed.
 __global__ void k_collect_overflow(Workspace W, int32_t* list, int32_t* count) {
     const int64_t rep = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (rep >= W.c.n) return;
-    if (W.fail[rep] == kFailHeap) list[atomicAdd(count, 1)] = static_cast<int32_t>(rep);
+    if (W.fail[rep] == kFailHeap || W.fail[rep] == kFailStack) list[atomicAdd(count, 1)] = static_cast<int32_t>(rep);
 }
 
 __global__ void k_export(Workspace W, DevRecord* rec, int64_t* busy) {
@@ -305,6 +308,8 @@ struct RuntimeImpl {
     bool ran = false;
     int64_t launches = 0;
     int64_t h2d_bytes = 0, d2h_bytes = 0;
+    bool spec_stack_limit1 = false;  // DSD_SPEC_STACK_LIMIT=1 (tests: force the HBM re-run)
+    bool smem_launch = false;  // the last launch ran the shared-memory variant (+ HBM re-run)
     // records cache (filled lazily after a collect run)
     bool rec_cached = false;
     std::vector<DevRecord> h_rec;
@@ -327,6 +332,7 @@ Runtime::Runtime(int device) : impl_(new RuntimeImpl) {
     DSD_CUDA(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking));
     if (const char* h = std::getenv("DSD_SMEM_HEAP")) impl_->smem_heap = std::max(0, std::atoi(h));
     if (const char* s = std::getenv("DSD_STEP_STATS")) impl_->step_stats = std::atoi(s) != 0;
+    if (const char* s = std::getenv("DSD_SPEC_STACK_LIMIT")) impl_->spec_stack_limit1 = std::atoi(s) == 1;
     if (const char* s = std::getenv("DSD_SPECIALIZE")) impl_->specialize = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_PLACEMENT")) impl_->placement = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_LANES_PER_WARP"))
@@ -591,6 +597,7 @@ void Runtime::launch() {
     }
     DSD_CUDA(cudaEventRecord(R.ev[1], R.stream));
     const bool smem = R.W.c.ns <= kSmemServers && R.smem_heap > 0;
+    R.smem_launch = smem;
     if (smem) {
         const size_t bytes = static_cast<size_t>(kBlock / kLanes) * smem_warp_bytes(R.W.c.ns, R.smem_heap, R.W.c.awc != 0);
         const int32_t* pcount = R.place_n ? static_cast<const int32_t*>(R.place.p) : nullptr;
@@ -612,7 +619,11 @@ void Runtime::launch() {
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-        if (spec)
+        DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false, true, false, 1>,
+                                      cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        if (spec && R.spec_stack_limit1)
+            k_simulate<true, false, true, false, 1><<<sgrid, kBlock, bytes, R.stream>>>(R.W, plist, pcount, R.smem_heap);
+        else if (spec)
             (R.step_stats ? k_simulate<true, true, true> : k_simulate<true, false, true>)<<<sgrid, kBlock, bytes, R.stream>>>(
                 R.W, plist, pcount, R.smem_heap);
         else if (R.W.c.awc)
@@ -650,6 +661,11 @@ void Runtime::sync() {
     RuntimeImpl& R = *impl_;
     DSD_CUDA(cudaSetDevice(R.device));
     DSD_CUDA(cudaStreamSynchronize(R.stream));
+    if (R.ran && R.n > 0 && R.smem_launch && std::getenv("DSD_HOST_TIMING")) {  // replicas the shared-memory kernel handed to the HBM variant
+        int32_t rerun = 0;
+        DSD_CUDA(cudaMemcpy(&rerun, R.ovf.p, sizeof(rerun), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "[dsd sync] re-run on the HBM variant: %d of %zu replicas\n", rerun, R.n);
+    }
     if (R.step_stats && R.W.step_stats) {
         unsigned long long s[64];
         DSD_CUDA(cudaMemcpy(s, R.stats.p, sizeof(s), cudaMemcpyDeviceToHost));

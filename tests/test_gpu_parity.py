@@ -2,6 +2,7 @@
 the same configs.  Bit-exact: every report byte (all integer outputs and the
 3/6-decimal float renderings), events_processed and end_time must match."""
 import os
+import re
 
 import pytest
 
@@ -123,6 +124,29 @@ def test_large_sweep_parallel_aggregation_matches_reference():
         assert (out.points, out.replicas, out.failed_points) == (1024, 768 * 7, 256)
         assert out.summary_json == js
         assert out.summary_csv == cs
+
+
+def test_specialized_stack_overflow_reruns_on_hbm_variant(capfd):
+    """The specialised kernel keeps a shorter action stack; a replica that
+    overflows it fails with kFailStack and runs again on the HBM variant.
+    DSD_SPEC_STACK_LIMIT=1 forces that for nearly every replica: the summaries
+    must not change."""
+    from paper_2511_21669_b200 import Simulator
+    spec = ("base: c1_single_pair.yaml\nseed: 5\nrepetitions: 3\naxes:\n"
+            "  policies.window.gamma: [1, 4, 9, 16]\n  network.rtt_ms: [2, 30]\n"
+            "  workload.acceptance_rate: [0.5, 0.9]\n  workload.rate_rps: [2, 40]\n")
+    js, cs = ref.run_sweep(spec, CFG, 4)
+    os.environ.update({"DSD_SPEC_STACK_LIMIT": "1", "DSD_HOST_TIMING": "1"})
+    try:
+        with Simulator(0) as s:
+            out = s.run_sweep(spec, base_dir=CFG)
+    finally:
+        del os.environ["DSD_SPEC_STACK_LIMIT"], os.environ["DSD_HOST_TIMING"]
+    err = capfd.readouterr().err
+    m = re.search(r"re-run on the HBM variant: (\d+) of (\d+) replicas", err)
+    assert m and int(m.group(1)) > int(m.group(2)) // 2, err[-2000:]
+    assert out.summary_json == js
+    assert out.summary_csv == cs
 
 
 @pytest.mark.parametrize("smem_heap", ["0", "2", "8"])
