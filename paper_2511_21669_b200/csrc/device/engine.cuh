@@ -486,8 +486,10 @@ struct Engine {
     int32_t fail = kFailNone;
     int32_t T, D;
     // action stack
-    uint32_t st0 = 0, st1 = 0, st2 = 0, st3 = 0;
-    int32_t sp = 0;
+    // slots hold kStackEmpty when unused (its kind bits read kActNone), so the
+    // depth needs no counter
+    static constexpr uint32_t kStackEmpty = 0xffffffffu;
+    uint32_t st0 = kStackEmpty, st1 = kStackEmpty, st2 = kStackEmpty, st3 = kStackEmpty;
     int32_t item_server = -1;
     // the one event a step schedules (pend_t < 0: none); step() inserts it
     // at its end, so the heap insertion is inlined once
@@ -624,7 +626,8 @@ struct Engine {
     // would need more fails with kFailStack and runs again on the HBM variant.
     DSD_HD int stack_cap() const { return spec ? kSpecStack : 4; }
     DSD_HD void push_act(uint32_t a) {
-        if (sp >= (spec ? spec_limit : 4)) {
+        const int lim = spec ? spec_limit : 4;  // full when the limit's last slot is taken
+        if ((lim <= 1 ? st0 : lim == 2 ? st1 : lim == 3 ? st2 : st3) != kStackEmpty) {
             fail = kFailStack;
             return;
         }
@@ -632,14 +635,13 @@ struct Engine {
         if (stack_cap() > 2) st2 = st1;
         st1 = st0;
         st0 = a;
-        ++sp;
     }
     DSD_HD uint32_t pop_act() {
         uint32_t a = st0;
         st0 = st1;
-        if (stack_cap() > 2) st1 = st2;
-        if (stack_cap() > 3) st2 = st3;
-        --sp;
+        st1 = stack_cap() > 2 ? st2 : kStackEmpty;
+        if (stack_cap() > 2) st2 = stack_cap() > 3 ? st3 : kStackEmpty;
+        if (stack_cap() > 3) st3 = kStackEmpty;
         return a;
     }
 
@@ -1372,7 +1374,7 @@ struct Engine {
     }
     // next_kind without the failure test (the kernel's chain loop tests it once per chain)
     DSD_HD uint32_t next_kind_unchecked() const {
-        if (sp > 0) return st0 & 15u;
+        if (st0 != kStackEmpty) return st0 & 15u;
         return (next_arr < N || heap_n > 0) ? static_cast<uint32_t>(kActPop) : static_cast<uint32_t>(kActNone);
     }
 
@@ -1445,10 +1447,10 @@ struct Engine {
 
     // Executes exactly one step of kind next_kind().
     DSD_HD void step() {
-        if (sp == 0) {
+        if (st0 == kStackEmpty) {
             pop_event();
             // a handler that is not a vote barrier runs in the same step
-            if (sp == 0 || is_barrier(st0 & 15u)) return;
+            if (st0 == kStackEmpty || is_barrier(st0 & 15u)) return;
         }
         const uint32_t a = pop_act();
         const uint32_t arg = a >> 4;
