@@ -521,7 +521,7 @@ struct Engine {
     const DevGrid *g_tp = nullptr, *g_td = nullptr, *g_dp = nullptr, *g_dd = nullptr;
     int64_t link_us = 0;
     // the warp's cooperative AWC scratch (shared memory), null for batches
-    // without AWC scenarios (decisions then run awc_predict on the lane)
+    // without AWC scenarios
     AwcWarpScratch* awc = nullptr;
 
     DSD_HD Engine(const Workspace& w, const DevScenario& s, int64_t replica, int32_t* server_base,
@@ -828,12 +828,13 @@ struct Engine {
                 }
                 return Decision{false, g};
             }
-            case 2: {  // AWC: extract_features -> predict_gamma -> stabilized_decide
-                int64_t p = pair_of(d, t);
-                double f[5];
-                extract_features(W, rep, p, t, SV(v_open, t), S.queue_capacity, link(d, t).rtt_ms, f);
-                return stabilized_decide(p, awc_predict(W.blob, S, f));
-            }
+            case 2:  // AWC: begin() hands these to the warp (extract_features ->
+                     // awc_serve_warp -> begin_awc); only batches with AWC
+                     // scenarios run them, on the kAwc kernels, so this is
+                     // unreachable - fail loudly rather than compile the
+                     // per-lane network into every kernel
+                fail = kFailAwcDims;
+                return Decision{true, 1};
             default:
                 return Decision{true, 1};
         }
