@@ -1,7 +1,8 @@
-"""Executed register moves (IMAD.MOV / MOV) of one k_simulate variant per
-source line, from an ncu --set full capture (see ncu_funcs.py).
+"""Executed register moves (IMAD.MOV / MOV) of one kernel per source line,
+from an ncu --set full capture (see ncu_funcs.py); with --all, every executed
+instruction per source line.
 
-  python tools/ncu_moves.py <report.ncu-rep> [variant-substring]
+  python tools/ncu_moves.py <report.ncu-rep> [kernel-substring] [--all]
 """
 import collections
 import csv
@@ -17,7 +18,8 @@ DEV = os.path.join(HERE, "paper_2511_21669_b200", "csrc", "device")
 LIB = os.path.join(HERE, "paper_2511_21669_b200", "libdsdsim.so")
 
 
-def main(rep, variant="k_simulateILb1ELb0ELb1ELb0"):
+def main(rep, variant="k_simulateILb1ELb0ELb1ELb0", *flags):
+    every = "--all" in flags
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -57,10 +59,10 @@ def main(rep, variant="k_simulateILb1ELb0ELb1ELb0"):
     for a, op, ex in data:
         ln = amap.get(a - base)
         allc[ln] += ex
-        if op.startswith("IMAD.MOV") or op == "MOV" or op.startswith("MOV."):
+        if every or op.startswith("IMAD.MOV") or op == "MOV" or op.startswith("MOV."):
             mv[ln] += ex
     tm = sum(mv.values())
-    print(f"moves: {100 * tm / tot:.1f}% of executed warp instructions")
+    print(f"{'all' if every else 'moves'}: {100 * tm / tot:.1f}% of executed warp instructions")
     for ln, ex in mv.most_common(30):
         text = ""
         if ln:
