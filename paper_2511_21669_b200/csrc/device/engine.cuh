@@ -689,6 +689,30 @@ struct Engine {
     DSD_HD void copy_rec(ReqRec& dst, const ReqRec& src) const {
         if (spec) copy_rec_inline(dst, src); else copy_rec_call(dst, src);
     }
+    // Specialised kernel: the active session's current acceptance-bit word,
+    // bits[cursor >> 6], kept in the 8 bytes that pad its shared-memory slot
+    // to kHotStride.  Refilled by an asynchronous global->shared copy when
+    // the session activates and when its cursor moves to another word, so a
+    // verify reads shared memory instead of a bit line that L1 (small next
+    // to the shared-memory carveout) has usually evicted.
+    DSD_HD uint64_t* slot_word() const { return reinterpret_cast<uint64_t*>(hotb + sizeof(ReqRec)); }
+    DSD_HD void fetch_word(const ReqRec& r, int32_t cur) const {
+#ifdef __CUDA_ARCH__
+        // a refill still in flight (the previous session's last verify) must
+        // land first: copies from one thread complete in no particular order
+        wait_word();
+        const uint64_t* src = W.bits + static_cast<int64_t>(rep) * W.c.bw + r.bitoff + (cur >> 6);
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(slot_word()));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+#else
+        *slot_word() = W.bits[static_cast<int64_t>(rep) * W.c.bw + r.bitoff + (cur >> 6)];
+#endif
+    }
+    static DSD_HD void wait_word() {
+#ifdef __CUDA_ARCH__
+        asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
+    }
     // pulls a queued session's record towards L2 ahead of its activation
     DSD_HD void prefetch_l2(int32_t i) const {
 #ifdef __CUDA_ARCH__
@@ -1077,6 +1101,7 @@ struct Engine {
         if (nx < 0) SV(v_stail, v) = -1;
         if (hot()) {
             copy_rec(slot(d), g);
+            if (spec && g.nbits > 0) fetch_word(g, g.cursor);
             prefetch_l2(nx);  // the next session's copy-in is one activation away
         }
         SV(v_active, v) = i;
@@ -1226,11 +1251,18 @@ struct Engine {
         const uint64_t* bits = W.bits + static_cast<int64_t>(rep) * W.c.bw + r.bitoff;
         const int32_t nb = r.nbits;
         int32_t cur = r.cursor;
+        const bool cached = spec && &r == &slot(0);  // the active session: its word is in the slot
         if (gamma > 0 && gamma <= 64 && cur + gamma <= nb) {
             // no wrap inside the window: the accepted prefix is the run of
             // trailing ones of the gamma bits at the cursor
             const int s = cur & 63;
-            uint64_t w = bits[cur >> 6] >> s;
+            uint64_t w;
+            if (cached) {
+                wait_word();
+                w = *slot_word() >> s;
+            } else {
+                w = bits[cur >> 6] >> s;
+            }
             if (s + gamma > 64) w |= bits[(cur >> 6) + 1] << (64 - s);
             const uint64_t zeros = ~w;
 #ifdef __CUDA_ARCH__
@@ -1240,12 +1272,16 @@ struct Engine {
 #endif
             accepted = ones < gamma ? ones : gamma;
             consumed = accepted < gamma ? accepted + 1 : gamma;
+            const int32_t old = cur;
             cur += consumed;
-            r.cursor = cur == nb ? 0 : cur;
+            cur = cur == nb ? 0 : cur;
+            r.cursor = cur;
+            if (cached && (cur >> 6) != (old >> 6)) fetch_word(r, cur);
             return;
         }
         accepted = 0;
         consumed = 0;
+        const int32_t old = cur;
         while (consumed < gamma) {
             uint64_t b = (bits[cur >> 6] >> (cur & 63)) & 1u;
             cur = cur + 1 == nb ? 0 : cur + 1;
@@ -1257,6 +1293,7 @@ struct Engine {
             }
         }
         r.cursor = cur;
+        if (cached && (cur >> 6) != (old >> 6)) fetch_word(r, cur);
     }
 
     // one member of a finished batch (engine.cpp:573-587, 591-646)
