@@ -309,7 +309,9 @@ struct RuntimeImpl {
     int64_t launches = 0;
     int64_t h2d_bytes = 0, d2h_bytes = 0;
     bool spec_stack_limit1 = false;  // DSD_SPEC_STACK_LIMIT=1 (tests: force the HBM re-run)
-    bool smem_launch = false;  // the last launch ran the shared-memory variant (+ HBM re-run)
+    bool smem_launch = false;
+    void* pinned = nullptr;  // host_summaries() buffer (page-locked)
+    size_t pinned_bytes = 0;  // the last launch ran the shared-memory variant (+ HBM re-run)
     // records cache (filled lazily after a collect run)
     bool rec_cached = false;
     std::vector<DevRecord> h_rec;
@@ -351,6 +353,7 @@ Runtime::~Runtime() {
     if (!impl_) return;
     cudaSetDevice(impl_->device);
     if (impl_->stream) cudaStreamSynchronize(impl_->stream);
+    if (impl_->pinned) cudaFreeHost(impl_->pinned);
     for (auto& ev : impl_->ev)
         if (ev) cudaEventDestroy(ev);
     if (impl_->stream) cudaStreamDestroy(impl_->stream);
@@ -705,7 +708,26 @@ void Runtime::summaries(dsd_replica_summary* out, size_t n) {
     DSD_CUDA(cudaStreamSynchronize(R.stream));
 }
 
+const dsd_replica_summary* Runtime::host_summaries() {
+    RuntimeImpl& R = *impl_;
+    if (!R.ran) throw Error(DSD_ERR_RUNTIME, "no completed batch");
+    DSD_CUDA(cudaSetDevice(R.device));
+    const size_t bytes = sizeof(DevSummary) * std::max<size_t>(R.n, 1);
+    if (bytes > R.pinned_bytes) {  // grown, never shrunk: later batches touch no fresh pages
+        if (R.pinned) DSD_CUDA(cudaFreeHost(R.pinned));
+        R.pinned = nullptr;
+        R.pinned_bytes = 0;
+        DSD_CUDA(cudaMallocHost(&R.pinned, bytes));
+        R.pinned_bytes = bytes;
+    }
+    if (R.n) DSD_CUDA(cudaMemcpyAsync(R.pinned, R.summary.p, sizeof(DevSummary) * R.n, cudaMemcpyDeviceToHost, R.stream));
+    R.d2h_bytes += static_cast<int64_t>(sizeof(DevSummary) * R.n);
+    DSD_CUDA(cudaStreamSynchronize(R.stream));
+    return static_cast<const dsd_replica_summary*>(R.pinned);
+}
+
 static_assert(kProbeFields == DSD_PROBE_FIELDS, "probe layout must match include/dsdsim.h");
+static_assert(sizeof(DevSummary) == sizeof(dsd_replica_summary), "summary layout must match include/dsdsim.h");
 
 void Runtime::probe(double* out, size_t n) {
     RuntimeImpl& R = *impl_;

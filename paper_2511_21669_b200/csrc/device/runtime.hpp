@@ -36,6 +36,9 @@ public:
     void launch();
     void sync();
     void summaries(dsd_replica_summary* out, size_t n);
+    // The batch's summaries in a page-locked buffer the Runtime owns (valid
+    // until the next call; no host allocation per batch).
+    const dsd_replica_summary* host_summaries();
     void fetch_records(size_t replica, dsd_request_record* records, size_t cap, int64_t* n_records,
                        int32_t* gamma_seq, int32_t* committed_seq, size_t seq_cap, int64_t* n_seq,
                        int64_t* busy_us, size_t busy_cap);

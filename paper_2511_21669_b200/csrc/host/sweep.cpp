@@ -13,6 +13,12 @@
 #include <iterator>
 #include <cstdlib>
 #include <thread>
+#include <unistd.h>
+#include <mutex>
+#include <memory>
+#include <functional>
+#include <exception>
+#include <condition_variable>
 
 #include "report.hpp"
 
@@ -114,8 +120,93 @@ static unsigned host_threads() {
     return t;
 }
 
+// Process-wide host worker threads for parallel_chunks: creating ~16 threads
+// costs a few hundred microseconds, several times per sweep.  One parallel
+// region at a time (a concurrent caller, e.g. a second handle on another
+// thread, spawns its own threads instead); recreated in a forked child.
+// Each region's task, counters and first exception live in a Region that
+// late-waking workers hold by shared_ptr, so they can never run a stale task.
+class HostPool {
+  public:
+    static HostPool* get(unsigned workers) {
+        static std::mutex mu;
+        static HostPool* pool = nullptr;
+        std::lock_guard<std::mutex> lk(mu);
+        if (!pool || pool->pid_ != getpid() || pool->workers_ < workers)
+            pool = new HostPool(workers);  // lives for the process (a replaced pool's threads stay parked)
+        return pool;
+    }
+    // task(0..tasks-1) on the workers and the caller; false when busy
+    bool try_run(size_t tasks, const std::function<void(size_t)>& task) {
+        std::unique_lock<std::mutex> busy(busy_, std::try_to_lock);
+        if (!busy) return false;
+        auto r = std::make_shared<Region>();
+        r->task = &task;
+        r->total = tasks;
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            region_ = r;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work(*r);
+        std::unique_lock<std::mutex> lk(r->m);
+        r->cv.wait(lk, [&] { return r->finished == r->total; });
+        if (r->err) std::rethrow_exception(r->err);
+        return true;
+    }
+
+  private:
+    struct Region {
+        const std::function<void(size_t)>* task = nullptr;
+        size_t total = 0;
+        std::atomic<size_t> next{0};
+        std::mutex m;
+        std::condition_variable cv;
+        size_t finished = 0;
+        std::exception_ptr err;
+    };
+    static void work(Region& r) {
+        size_t did = 0;
+        for (size_t i; (i = r.next.fetch_add(1)) < r.total; ++did) {
+            try {
+                (*r.task)(i);
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(r.m);
+                if (!r.err) r.err = std::current_exception();
+            }
+        }
+        if (did == 0) return;
+        std::lock_guard<std::mutex> lk(r.m);
+        r.finished += did;
+        if (r.finished == r.total) r.cv.notify_all();
+    }
+    explicit HostPool(unsigned workers) : workers_(workers), pid_(getpid()) {
+        for (unsigned w = 0; w < workers; ++w)
+            std::thread([this] {
+                uint64_t seen = 0;
+                for (;;) {
+                    std::shared_ptr<Region> r;
+                    {
+                        std::unique_lock<std::mutex> lk(m_);
+                        cv_.wait(lk, [&] { return gen_ != seen; });
+                        seen = gen_;
+                        r = region_;
+                    }
+                    work(*r);
+                }
+            }).detach();
+    }
+    unsigned workers_;
+    pid_t pid_;
+    std::mutex busy_, m_;
+    std::condition_variable cv_;
+    uint64_t gen_ = 0;
+    std::shared_ptr<Region> region_;
+};
+
 // fn(begin, end) over contiguous chunks of [0, n), at least `grain` items per
-// thread; the calling thread takes the first chunk.
+// chunk; the calling thread takes part.
 template <class F>
 static void parallel_chunks(size_t n, size_t grain, F&& fn) {
     const size_t t = std::min<size_t>(host_threads(), std::max<size_t>(1, n / std::max<size_t>(grain, 1)));
@@ -123,10 +214,12 @@ static void parallel_chunks(size_t n, size_t grain, F&& fn) {
         fn(size_t{0}, n);
         return;
     }
+    const std::function<void(size_t)> chunk = [&fn, n, t](size_t i) { fn(n * i / t, n * (i + 1) / t); };
+    if (HostPool::get(static_cast<unsigned>(t - 1))->try_run(t, chunk)) return;
     std::vector<std::thread> pool;
     pool.reserve(t - 1);
-    for (size_t i = 1; i < t; ++i) pool.emplace_back([&fn, n, t, i] { fn(n * i / t, n * (i + 1) / t); });
-    fn(size_t{0}, n / t);
+    for (size_t i = 1; i < t; ++i) pool.emplace_back([&chunk, i] { chunk(i); });
+    chunk(0);
     for (auto& th : pool) th.join();
 }
 
@@ -249,11 +342,11 @@ void collect_batch(Runtime& rt, SweepBatch& b, const std::string& out_dir, Sweep
     PhaseTimer tm("run_sweep");
     const bool reports = !out_dir.empty();
     const size_t n = b.replicas.size();
-    std::vector<dsd_replica_summary> sums(n);
+    const dsd_replica_summary* sums = nullptr;
     if (n > 0) {
         rt.sync();
         tm.lap("kernels");
-        rt.summaries(sums.data(), n);
+        sums = rt.host_summaries();
         tm.lap("summaries");
     }
     const int R = b.spec.repetitions;
