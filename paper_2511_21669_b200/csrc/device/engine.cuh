@@ -928,7 +928,7 @@ struct Engine {
     // try_dispatch (engine.cpp:485-567)
     DSD_HD void try_dispatch(int32_t v, bool window_expired) {
         if (busy(v) || SV(v_qhead, v) < 0) return;
-        if (spec && v == 1 && dispatch_single_draft()) return;
+        if (spec && (v == 1 ? dispatch_single_draft() : dispatch_single_target())) return;
         const bool is_draft = v >= T;
         const int64_t mb = is_draft ? dmax_batch : max_batch;
         int32_t kind = -1;
@@ -1040,6 +1040,46 @@ struct Engine {
         set_busy_flag(v, true);
         if (!is_draft) set_busy(v, get_busy(v) + lat);  // only target busy time is reported
         defer(now + lat, info(kEvComputeDone, 0, static_cast<uint32_t>(v)));
+    }
+
+    // try_dispatch of the specialised kernel's target server when its queue
+    // holds one item (with one draft server, only the active session has
+    // work at the target): FIFO forming takes that item if it is eligible
+    // (item_eligible) and nothing otherwise; same BatchShape, latency query,
+    // rounding and busy time as the general pass with taken = 1.
+    DSD_HD bool dispatch_single_target() {
+        const int32_t cur = SV(v_qhead, 0);
+        ReqRec& r = rec(cur >> 1);
+        const int k = cur & 1;
+        if (r.next[k] >= 0) return false;  // more than one item: the general path
+        const uint32_t opv = r.op[k];
+        const uint32_t op = opv & 3u;
+        if (!eligible(false, op, r)) return true;  // nothing eligible: no batch
+        SV(v_qhead, 0) = -1;
+        SV(v_qtail, 0) = -1;
+        SV(v_run, 0) = cur;
+        const int32_t t_i = k ? r.tok1 : r.prompt;
+        const int32_t tok = t_i > 1 ? t_i : 1;
+        const bool prefill = op == kOpPrefill;
+        const bool decode = op == kOpDecode;
+        const int64_t ctx = prefill ? 0 : static_cast<int64_t>(r.prompt) + r.tokens;
+        if (opv & 4u) {
+            net_wait_total += now - r.enq[k];
+            ++net_wait_count;
+        }
+        const int64_t qb = (prefill || decode) ? 1 : tok;
+        const int64_t qc = prefill ? static_cast<int64_t>(tok) : (ctx > 0 ? ctx : 0);
+        const DevGrid& g = *(prefill ? g_tp : g_td);
+        double ms = g.o_btab >= 0 && g.o_ctab >= 0 ? grid_interpolate_int(W.blob, g, qb, qc)
+                                                    : grid_interpolate(W.blob, g, static_cast<double>(qb),
+                                                                       static_cast<double>(qc));
+        if (decode) ms *= tok;
+        int64_t lat = llround(ms * 1000.0);
+        if (lat < 1) lat = 1;
+        set_busy_flag(0, true);
+        set_busy(0, get_busy(0) + lat);
+        defer(now + lat, info(kEvComputeDone, 0, 0u));
+        return true;
     }
 
     // try_dispatch of the specialised kernel's draft server when its queue
