@@ -1,8 +1,9 @@
 """Executed register moves (IMAD.MOV / MOV) of one kernel per source line,
 from an ncu --set full capture (see ncu_funcs.py); with --all, every executed
-instruction per source line.
+instruction per source line; with --stall=<reason> (long_sb, wait, ...), that
+reason's warp-stall samples per source line.
 
-  python tools/ncu_moves.py <report.ncu-rep> [kernel-substring] [--all]
+  python tools/ncu_moves.py <report.ncu-rep> [kernel-substring] [--all | --stall=long_sb]
 """
 import collections
 import csv
@@ -20,6 +21,7 @@ LIB = os.path.join(HERE, "paper_2511_21669_b200", "libdsdsim.so")
 
 def main(rep, variant="k_simulateILb1ELb0ELb1ELb0", *flags):
     every = "--all" in flags
+    stall = next((f.split("=", 1)[1] for f in flags if f.startswith("--stall=")), None)
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -29,7 +31,7 @@ def main(rep, variant="k_simulateILb1ELb0ELb1ELb0", *flags):
     for r in rows[hi + 1:]:
         try:
             a = int(r[ix["Address"]], 16)
-            ex = float(r[ix["Instructions Executed"]] or 0)
+            ex = float(r[ix["stall_" + stall if stall else "Instructions Executed"]] or 0)
         except (ValueError, IndexError):
             continue
         t = r[ix["Source"]].split()
@@ -59,10 +61,11 @@ def main(rep, variant="k_simulateILb1ELb0ELb1ELb0", *flags):
     for a, op, ex in data:
         ln = amap.get(a - base)
         allc[ln] += ex
-        if every or op.startswith("IMAD.MOV") or op == "MOV" or op.startswith("MOV."):
+        if every or stall or op.startswith("IMAD.MOV") or op == "MOV" or op.startswith("MOV."):
             mv[ln] += ex
     tm = sum(mv.values())
-    print(f"{'all' if every else 'moves'}: {100 * tm / tot:.1f}% of executed warp instructions")
+    what = f"stall_{stall} samples" if stall else ("all" if every else "moves")
+    print(f"{what}: {100 * tm / tot:.1f}% (of the column total)")
     for ln, ex in mv.most_common(30):
         text = ""
         if ln:
