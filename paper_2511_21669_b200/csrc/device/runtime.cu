@@ -294,6 +294,7 @@ struct RuntimeImpl {
     // -1] (empty: replica = thread index)
     DevBuf place;
     int64_t place_n = 0;
+    bool place_pending = false;  // prepare() -> the next launch() computes the placement
     int lanes_per_warp = 32;  // env DSD_LANES_PER_WARP: replicas per warp (experiments)
     bool placement = true;    // cost-aware lane placement (env DSD_PLACEMENT=0 disables)
     int sms = 148, smem_per_sm = 228 * 1024;
@@ -517,9 +518,27 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
         R.spec_ok = R.spec_ok && d.n_targets == 1 && d.n_drafts == 1 && !d.fused_everything && d.window_kind == 0 &&
                     d.batching == 0 && d.batching_window_us == 0 && d.jitter_free && d.n_dg == 1 && d.n_tg == 1 &&
                     !d.has_order && !d.pair_stats;
-    const bool spec_launch = R.spec_ok && R.specialize && !collect && !feature_probe;
+    // the lane placement is computed by launch() while k_stage runs
+    R.place_pending = true;
+    R.n = n;
+    R.collect = collect;
+    if (collect) R.ltot.ensure(sizeof(int64_t) * std::max<size_t>(n, 1));
+    lap("workspace");
+    DSD_CUDA(cudaStreamSynchronize(R.stream));
+    lap("sync");
+    R.prepared = true;
+}
+
+// Lane placement of the prepared batch (placement_list, or the uniform
+// DSD_LANES_PER_WARP layout), uploaded on the stream: launch() computes it on
+// the host while k_stage runs, once per prepared batch.
+static void place_lanes(RuntimeImpl& R) {
+    R.place_pending = false;
+    R.place_n = 0;
+    const size_t n = R.n;
+    const bool spec_launch = R.spec_ok && R.specialize && !R.collect && !R.W.probe;
     const int64_t max_blocks = spec_launch ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_BLOCKS;
-    std::vector<int32_t> pl = placement_list(P, n, R.sms * max_blocks * (kBlock / kLanes));
+    std::vector<int32_t> pl = placement_list(R.packed, n, R.sms * max_blocks * (kBlock / kLanes));
     if (!pl.empty() && R.placement && R.lanes_per_warp == kLanes) {
         R.place.ensure(4 * pl.size());
         DSD_CUDA(cudaMemcpyAsync(R.place.p, pl.data(), 4 * pl.size(), cudaMemcpyHostToDevice, R.stream));
@@ -528,22 +547,15 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
     if (R.lanes_per_warp < kLanes && n > 0) {
         const int64_t lpw = R.lanes_per_warp;
         const int64_t nw = (static_cast<int64_t>(n) + lpw - 1) / lpw;
-        std::vector<int32_t> pl(static_cast<size_t>(nw * kLanes + 1), -1);
-        pl[0] = static_cast<int32_t>(nw * kLanes);
+        std::vector<int32_t> ul(static_cast<size_t>(nw * kLanes + 1), -1);
+        ul[0] = static_cast<int32_t>(nw * kLanes);
         for (int64_t w = 0; w < nw; ++w)
             for (int64_t l = 0; l < lpw; ++l)
-                if (w * lpw + l < static_cast<int64_t>(n)) pl[1 + w * kLanes + l] = static_cast<int32_t>(w * lpw + l);
-        R.place.ensure(4 * pl.size());
-        DSD_CUDA(cudaMemcpyAsync(R.place.p, pl.data(), 4 * pl.size(), cudaMemcpyHostToDevice, R.stream));
+                if (w * lpw + l < static_cast<int64_t>(n)) ul[1 + w * kLanes + l] = static_cast<int32_t>(w * lpw + l);
+        R.place.ensure(4 * ul.size());
+        DSD_CUDA(cudaMemcpyAsync(R.place.p, ul.data(), 4 * ul.size(), cudaMemcpyHostToDevice, R.stream));
         R.place_n = nw * kLanes;
     }
-    R.n = n;
-    R.collect = collect;
-    if (collect) R.ltot.ensure(sizeof(int64_t) * std::max<size_t>(n, 1));
-    lap("workspace");
-    DSD_CUDA(cudaStreamSynchronize(R.stream));
-    lap("sync");
-    R.prepared = true;
 }
 
 void Runtime::launch() {
@@ -573,6 +585,7 @@ void Runtime::launch() {
                                            nullptr);
     DSD_CUDA(cudaGetLastError());
     ++R.launches;
+    if (R.place_pending) place_lanes(R);
     if (R.collect) {
         // size the sequence arena exactly: prefix sum of per-replica output totals
         R.host_ltot.resize(R.n);
