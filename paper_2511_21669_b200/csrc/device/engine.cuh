@@ -177,7 +177,7 @@ struct AwcWarpScratch {
 #ifdef __CUDACC__
 // WcDnn::forward (mlp.cpp:83-97) of one lane's request, evaluated by the whole
 // warp: each output row is one lane's avx2_dot in the reference's order, so
-// the result is bit-identical to awc_predict; the vectors are broadcast
+// the result is bit-identical to awc_forward_lane; the vectors are broadcast
 // through shared memory.  Every lane of the warp must call it (converged).
 __device__ __noinline__ double awc_forward_warp(const char* blob, const DevScenario* S, const double* x,
                                                 AwcWarpScratch* sc) {
@@ -277,14 +277,6 @@ __device__ __forceinline__ void awc_serve_warp(const char* blob, const DevScenar
     }
 }
 #endif
-
-// out of line: ~34K flops per call, called once per AWC decision; keeping it
-// out of the event loop keeps the loop small enough for the instruction cache
-DSD_HD double awc_predict(const char* blob, const DevScenario& S, const double raw[5]) {
-    double x[5];
-    awc_normalize(S, raw, x);
-    return awc_forward_lane(blob, S, x);
-}
 
 // WcDnn::forward (mlp.cpp:83-97) by one thread on a normalised input
 DSD_HD_NOINLINE double awc_forward_lane(const char* blob, const DevScenario& S, const double* x) {
