@@ -101,6 +101,22 @@ def test_sweep_report_files_match_reference(sim, tmp_path):
         assert (ref_dir / f).read_bytes() == (my_dir / f).read_bytes(), f
 
 
+def test_full_c5_sweep_matches_reference():
+    """The benchmark workload itself at full size: the 65,536-replica C5 sweep
+    (4,096 points x 16 repetitions, 8.8e8 events) through dsd_run_sweep must
+    give the reference run_sweep's summary JSON/CSV byte for byte (the
+    reference runs on all host cores, ~10 s)."""
+    from paper_2511_21669_b200 import Simulator
+    spec = open(os.path.join(CFG, "c5_sweep_65536.yaml")).read()
+    js, cs = ref.run_sweep(spec, CFG, os.cpu_count() or 8)
+    with Simulator(0) as s:
+        out = s.run_sweep(spec, base_dir=CFG)
+    assert (out.points, out.replicas, out.failed_points) == (4096, 65536, 0)
+    assert out.events_processed == 880021538
+    assert out.summary_json == js
+    assert out.summary_csv == cs
+
+
 def test_large_sweep_parallel_aggregation_matches_reference():
     """A sweep above the host's parallel thresholds (4,096 replicas for the
     per-point sums, 1,024 points for the summary text): sums split across host
