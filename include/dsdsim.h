@@ -33,6 +33,10 @@
  *   - A handle drives exactly one CUDA device and must be used from one host
  *     thread at a time (the reference Engine is single-threaded too,
  *     SPEC.md:76).  Multi-GPU runs create one handle per device/process.
+ *     Internally the sweep planning and summary loops run on a process-wide
+ *     pool of host worker threads (DSD_HOST_THREADS), and dsd_run_sweep frees
+ *     its host batch on a helper thread that the next call or dsd_destroy
+ *     joins; neither is visible through the ABI.
  *   - There is no CPU fallback: every simulation runs in the sm_100a kernels.
  *     Creating a handle without a usable GPU fails with DSD_ERR_RUNTIME.
  */
