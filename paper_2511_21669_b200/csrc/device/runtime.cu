@@ -297,6 +297,7 @@ struct RuntimeImpl {
     bool place_pending = false;  // prepare() -> the next launch() computes the placement
     int lanes_per_warp = 32;  // env DSD_LANES_PER_WARP: replicas per warp (experiments)
     bool placement = true;    // cost-aware lane placement (env DSD_PLACEMENT=0 disables)
+    bool spread = true;       // sparse batches over the whole wave (env DSD_SPREAD=0 disables)
     int sms = 148, smem_per_sm = 228 * 1024;
     DevBuf stats;
     Workspace W{};
@@ -338,6 +339,7 @@ Runtime::Runtime(int device) : impl_(new RuntimeImpl) {
     if (const char* s = std::getenv("DSD_SPEC_STACK_LIMIT")) impl_->spec_stack_limit1 = std::atoi(s) == 1;
     if (const char* s = std::getenv("DSD_SPECIALIZE")) impl_->specialize = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_PLACEMENT")) impl_->placement = std::atoi(s) != 0;
+    if (const char* s = std::getenv("DSD_SPREAD")) impl_->spread = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_LANES_PER_WARP"))
         impl_->lanes_per_warp = std::max(1, std::min(kLanes, std::atoi(s)));
     if (const char* s = std::getenv("DSD_CARVEOUT")) {  // shared-memory share of the L1/smem array (%)
@@ -544,8 +546,28 @@ static void place_lanes(RuntimeImpl& R) {
         DSD_CUDA(cudaMemcpyAsync(R.place.p, pl.data(), 4 * pl.size(), cudaMemcpyHostToDevice, R.stream));
         R.place_n = static_cast<int64_t>(pl.size()) - 1;
     }
-    if (R.lanes_per_warp < kLanes && n > 0) {
-        const int64_t lpw = R.lanes_per_warp;
+    // A batch that leaves most SMs idle when dense (at most one full warp per
+    // SM) and that the cost-aware placement does not place (any workload but
+    // synthetic static windows; e.g. the AWC dataset's 2,400 replicas = 75
+    // warps on 148 SMs): spread it over the wave, ceil(n / warp capacity)
+    // replicas per warp - every SM gets work and fewer lanes share a warp's
+    // vote rounds (dataset 118 -> 58 ms, a 768-replica AWC sweep 1.97 ->
+    // 0.32 s).  Denser batches stay dense: spreading a 24,576-replica
+    // dynamic-window sweep made it 14% slower.
+    int64_t lpw = R.lanes_per_warp;
+    if (R.place_n == 0 && R.placement && lpw == kLanes && n > 0 && R.spread &&
+        static_cast<int64_t>(n) <= static_cast<int64_t>(R.sms) * kLanes) {
+        const bool smem = R.W.c.ns <= kSmemServers && R.smem_heap > 0;
+        int64_t per_sm = max_blocks;
+        if (smem) {
+            const int64_t bytes = (kBlock / kLanes) * smem_warp_bytes(spec_launch ? 2 : R.W.c.ns, R.smem_heap,
+                                                                      R.W.c.awc != 0);
+            per_sm = std::max<int64_t>(1, std::min<int64_t>(max_blocks, R.smem_per_sm / (bytes + 1024)));
+        }
+        const int64_t cap = R.sms * per_sm * (kBlock / kLanes);
+        lpw = std::max<int64_t>(1, (static_cast<int64_t>(n) + cap - 1) / cap);
+    }
+    if (lpw < kLanes && n > 0) {
         const int64_t nw = (static_cast<int64_t>(n) + lpw - 1) / lpw;
         std::vector<int32_t> ul(static_cast<size_t>(nw * kLanes + 1), -1);
         ul[0] = static_cast<int32_t>(nw * kLanes);
@@ -573,13 +595,16 @@ void Runtime::launch() {
     // carveout keeps just that (the rest of the array is L1, which holds the
     // AWC weights and the replicas' state)
     const size_t hbm_smem = R.W.c.awc ? (kBlock / kLanes) * sizeof(AwcWarpScratch) : 0;
-    if (R.carveout < 0) {
-        const int64_t per_sm = std::min<int64_t>(DSD_MIN_BLOCKS, (grid + R.sms - 1) / R.sms);
+    // sized for the blocks a launch of `g` blocks puts on an SM
+    auto hbm_carveout = [&](unsigned g) {
+        if (R.carveout >= 0) return;
+        const int64_t per_sm = std::min<int64_t>(DSD_MIN_BLOCKS, (g + R.sms - 1) / R.sms);
         const int64_t need = hbm_smem ? per_sm * (static_cast<int64_t>(hbm_smem) + 1024) : 0;
         const int pct = static_cast<int>(std::min<int64_t>(100, (100 * need + R.smem_per_sm - 1) / R.smem_per_sm));
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<false, false, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
-    }
+    };
+    hbm_carveout(grid);
     DSD_CUDA(cudaEventRecord(R.ev[0], R.stream));
     k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, R.collect ? static_cast<int64_t*>(R.ltot.p) : nullptr, nullptr,
                                            nullptr);
@@ -664,8 +689,13 @@ void Runtime::launch() {
         DSD_CUDA(cudaGetLastError());
         R.launches += 4;
     } else {
+        // (HBM state is indexed by replica, so a lane placement is just a thread -> replica list)
+        const int32_t* pcount = R.place_n ? static_cast<const int32_t*>(R.place.p) : nullptr;
+        const int32_t* plist = R.place_n ? pcount + 1 : nullptr;
+        const unsigned hgrid = R.place_n ? static_cast<unsigned>((R.place_n + kBlock - 1) / kBlock) : grid;
+        if (hgrid != grid) hbm_carveout(hgrid);
         (R.W.c.awc ? (R.step_stats ? k_simulate<false, true, false, true> : k_simulate<false, false, false, true>)
-                    : (R.step_stats ? k_simulate<false, true> : k_simulate<false, false>))<<<grid, kBlock, hbm_smem, R.stream>>>(R.W, nullptr, nullptr, 0);
+                    : (R.step_stats ? k_simulate<false, true> : k_simulate<false, false>))<<<hgrid, kBlock, hbm_smem, R.stream>>>(R.W, plist, pcount, 0);
         DSD_CUDA(cudaGetLastError());
         ++R.launches;
     }
