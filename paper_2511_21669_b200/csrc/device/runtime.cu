@@ -298,6 +298,7 @@ struct RuntimeImpl {
     int lanes_per_warp = 32;  // env DSD_LANES_PER_WARP: replicas per warp (experiments)
     bool placement = true;    // cost-aware lane placement (env DSD_PLACEMENT=0 disables)
     bool spread = true;       // sparse batches over the whole wave (env DSD_SPREAD=0 disables)
+    double spread_max = 2.5;  // ... up to this many dense warps per SM (env DSD_SPREAD_MAX)
     int sms = 148, smem_per_sm = 228 * 1024;
     DevBuf stats;
     Workspace W{};
@@ -340,6 +341,7 @@ Runtime::Runtime(int device) : impl_(new RuntimeImpl) {
     if (const char* s = std::getenv("DSD_SPECIALIZE")) impl_->specialize = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_PLACEMENT")) impl_->placement = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_SPREAD")) impl_->spread = std::atoi(s) != 0;
+    if (const char* s = std::getenv("DSD_SPREAD_MAX")) impl_->spread_max = std::atof(s);
     if (const char* s = std::getenv("DSD_LANES_PER_WARP"))
         impl_->lanes_per_warp = std::max(1, std::min(kLanes, std::atoi(s)));
     if (const char* s = std::getenv("DSD_CARVEOUT")) {  // shared-memory share of the L1/smem array (%)
@@ -546,17 +548,17 @@ static void place_lanes(RuntimeImpl& R) {
         DSD_CUDA(cudaMemcpyAsync(R.place.p, pl.data(), 4 * pl.size(), cudaMemcpyHostToDevice, R.stream));
         R.place_n = static_cast<int64_t>(pl.size()) - 1;
     }
-    // A batch that leaves most SMs idle when dense (at most one full warp per
-    // SM) and that the cost-aware placement does not place (any workload but
-    // synthetic static windows; e.g. the AWC dataset's 2,400 replicas = 75
-    // warps on 148 SMs): spread it over the wave, ceil(n / warp capacity)
-    // replicas per warp - every SM gets work and fewer lanes share a warp's
-    // vote rounds (dataset 118 -> 58 ms, a 768-replica AWC sweep 1.97 ->
-    // 0.32 s).  Denser batches stay dense: spreading a 24,576-replica
-    // dynamic-window sweep made it 14% slower.
+    // A batch that leaves the SMs underfilled when dense (at most 2.5 full
+    // warps per SM) and that the cost-aware placement does not place (any
+    // workload but synthetic static windows; e.g. the AWC dataset's 2,400
+    // replicas = 75 warps on 148 SMs): spread it over the wave, ceil(n / warp
+    // capacity) replicas per warp - every SM gets work and fewer lanes share a
+    // warp's vote rounds.  Measured: dataset 118 -> 58 ms, a 768-replica AWC
+    // sweep 1.97 -> 0.32 s, dynamic-window sweeps of 2,048 / 4,096 / 8,192 /
+    // 12,288 replicas -24 / -20 / -9 / -2%, but 24,576 replicas +12%.
     int64_t lpw = R.lanes_per_warp;
     if (R.place_n == 0 && R.placement && lpw == kLanes && n > 0 && R.spread &&
-        static_cast<int64_t>(n) <= static_cast<int64_t>(R.sms) * kLanes) {
+        static_cast<double>(n) <= R.spread_max * R.sms * kLanes) {
         const bool smem = R.W.c.ns <= kSmemServers && R.smem_heap > 0;
         int64_t per_sm = max_blocks;
         if (smem) {
