@@ -1442,10 +1442,13 @@ struct Engine {
         if (fail) return kActNone;
         return next_kind_unchecked();
     }
-    // next_kind without the failure test (the kernel's chain loop tests it once per chain)
+    // next_kind for the chain loop: a failed replica finishes the (at most two)
+    // pending actions - every failure leaves the state bounded: a dropped push
+    // or heap insertion, a guarded arena write - and stops at its next pop
     DSD_HD uint32_t next_kind_unchecked() const {
         if (st0 != kStackEmpty) return st0 & 15u;
-        return (next_arr < N || heap_n > 0) ? static_cast<uint32_t>(kActPop) : static_cast<uint32_t>(kActNone);
+        return (!fail && (next_arr < N || heap_n > 0)) ? static_cast<uint32_t>(kActPop)
+                                                       : static_cast<uint32_t>(kActNone);
     }
 
     // SimKernel::run_until's pop (event_queue.cpp:28-42): a 2-way merge of the

@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_
                 }
                 kind = e.next_kind_unchecked();
             } while (!((kBarrierKinds >> kind) & 1u));
-            if (e.fail) kind = kActNone;  // a failed replica stops (checked once per chain)
+            // (a failed replica stops at its next pop: next_kind_unchecked)
         }
         if constexpr (kStats) ++iters;
     }
