@@ -56,14 +56,19 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """dram read+write bytes per simulate-kernel launch from the committed ncu capture, if any."""
+def ncu_summary():
+    """The committed ncu --set full summary of the simulate kernel (profiles/), if any."""
     p = os.path.join(REPO, "profiles", "ncu_sim_kernel.json")
     try:
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            return json.load(f)
     except Exception:
-        return None
+        return {}
+
+
+def ncu_traffic():
+    """dram read+write bytes per simulate-kernel launch from the committed ncu capture, if any."""
+    return ncu_summary().get("dram_bytes_per_launch")
 
 
 class Clocks:
@@ -318,7 +323,11 @@ def main_ours(args, rank, world, local_rank):
                 "path": "dsd_run_sweep" if world == 1 else "dsd_prepare_sweep+dsd_batch_launch+dsd_batch_summaries"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_kind, "bytes_per_event": B_EV,
-                     "kernel": "k_simulate", "kernel_ms": sim_avg},
+                     "kernel": "k_simulate", "kernel_ms": sim_avg,
+                     # the DES is latency-bound, not HBM-bound: the
+                     # committed capture's SM issue activity and top warp stalls
+                     "ncu_issue_active_pct": ncu_summary().get("issue_active_pct"),
+                     "ncu_stall_pct": dict(list(ncu_summary().get("stall_pct", {}).items())[:4])},
         "gpu_launches": sim.last_launch_count() * args.steps,
         "wall_s": wall,
     }
