@@ -99,6 +99,27 @@ DSD_HD_NOINLINE double grid_interpolate(const char* blob, const DevGrid& g, doub
     return r * g.calibration;
 }
 
+// LatencyProfile::predict (profile.cpp:129-151) on one grid for an integer
+// query, times `mult` tokens when mult > 0 (decode), as ms_to_us with the
+// engine's 1 us floor (engine.cpp:553-557)
+DSD_HD int64_t grid_latency_us(const char* blob, const DevGrid& g, int64_t qb, int64_t qc, int32_t mult) {
+    double ms = g.o_btab >= 0 && g.o_ctab >= 0
+                    ? grid_interpolate_int(blob, g, qb, qc)
+                    : grid_interpolate(blob, g, static_cast<double>(qb), static_cast<double>(qc));
+    if (mult > 0) ms *= mult;
+    const int64_t lat = llround(ms * 1000.0);
+    return lat < 1 ? 1 : lat;
+}
+
+// A session latency table of the specialised kernel (Workspace::spec_lat):
+// draft decode grid, verify grid, gamma (>= 1), contexts [0, n), and its
+// element offset (status word, pad, then n {draft, verify} pairs).
+struct SpecLatJob {
+    int64_t o_gd, o_gt, base;
+    int32_t g1, n;
+};
+constexpr int32_t kSpecLatMax = 1 << 28;  // entries must stay below (32-bit relative times)
+
 // ---------------------------------------------------------------------------
 // AWC: FeatureNormalizer::transform + WcDnn::forward (mlp.cpp:83-97,163-176)
 // with Backend::matvec in the AVX2 summation order the reference auto-selects
@@ -1034,6 +1055,10 @@ struct Engine {
         defer(now + lat, info(kEvComputeDone, 0, static_cast<uint32_t>(v)));
     }
 
+    DSD_HD int64_t latency_us(const DevGrid& g, int64_t qb, int64_t qc, int32_t mult) const {
+        return grid_latency_us(W.blob, g, qb, qc, mult);
+    }
+
     // try_dispatch of the specialised kernel's target server when its queue
     // holds one item (with one draft server, only the active session has
     // work at the target): FIFO forming takes that item if it is eligible
@@ -1061,13 +1086,7 @@ struct Engine {
         }
         const int64_t qb = (prefill || decode) ? 1 : tok;
         const int64_t qc = prefill ? static_cast<int64_t>(tok) : (ctx > 0 ? ctx : 0);
-        const DevGrid& g = *(prefill ? g_tp : g_td);
-        double ms = g.o_btab >= 0 && g.o_ctab >= 0 ? grid_interpolate_int(W.blob, g, qb, qc)
-                                                    : grid_interpolate(W.blob, g, static_cast<double>(qb),
-                                                                       static_cast<double>(qc));
-        if (decode) ms *= tok;
-        int64_t lat = llround(ms * 1000.0);
-        if (lat < 1) lat = 1;
+        const int64_t lat = latency_us(*(prefill ? g_tp : g_td), qb, qc, decode ? tok : 0);
         set_busy_flag(0, true);
         set_busy(0, get_busy(0) + lat);
         defer(now + lat, info(kEvComputeDone, 0, 0u));
@@ -1092,13 +1111,9 @@ struct Engine {
         const bool prefill = op == kOpPrefill;
         const int64_t ctx = prefill ? 0 : static_cast<int64_t>(r.prompt) + r.tokens;
         // qb = taken = 1 (prefill / decode); qc = prompt tokens / context
-        const DevGrid& g = *(prefill ? g_dp : g_dd);
         const int64_t qc = prefill ? static_cast<int64_t>(tok) : (ctx > 0 ? ctx : 0);
-        double ms = g.o_btab >= 0 && g.o_ctab >= 0 ? grid_interpolate_int(W.blob, g, 1, qc)
-                                                    : grid_interpolate(W.blob, g, 1.0, static_cast<double>(qc));
-        if (!prefill) ms *= tok;  // decode: latency x tokens_per_request
-        int64_t lat = llround(ms * 1000.0);
-        if (lat < 1) lat = 1;
+        // decode: latency x tokens_per_request
+        const int64_t lat = latency_us(*(prefill ? g_dp : g_dd), 1, qc, prefill ? 0 : tok);
         set_busy_flag(1, true);
         defer(now + lat, info(kEvComputeDone, 0, 1u));
         return true;
@@ -1242,6 +1257,227 @@ struct Engine {
             r.pgamma = dec.gamma;
             set_phase(r, kPhSpeculating);
             enqueue(T + d, i, 1, kOpDecode, dec.gamma, false);
+        }
+    }
+
+    // Specialised kernel: the active session's speculation loop run directly.
+    // One iteration is five events - IterationStart (begin_iteration + the
+    // draft's dispatch), the draft's ComputeDone (send_proposal), the
+    // proposal's NetArrive (verify enqueued and dispatched), the target's
+    // ComputeDone (consume_acceptance, the result sent back) and the result's
+    // NetArrive (commit_tokens, the next IterationStart at the same time).
+    // Each of them is scheduled by its predecessor, so it carries the largest
+    // seq so far: it is the replica's next event exactly when its time is
+    // below `ext`, the earliest of the next arrival (seq < N) and the heap top
+    // (scheduled earlier).  While that holds no other event runs, the heap
+    // and both servers' queues stay as they were, and the event is handled
+    // here without a heap round trip, an action-stack round trip or a warp
+    // vote; seq_next advances as its schedule() would.  The first event that
+    // is not the earliest goes to the heap through defer() (the same seq),
+    // and anything the loop does not cover (a busy or non-empty target, the
+    // target prefill still pending, the request finishing) is handed to the
+    // general handlers in the state they would have reached, so events,
+    // seqs, timestamps and totals are identical to the step-by-step path.
+    //
+    // The request's evolving fields live in registers for the loop and are
+    // written back once at its exit.  Both latency queries of an iteration
+    // use the same context (prompt + tokens committed so far), and the
+    // verify's acceptance draw only depends on the cursor, so the two
+    // bilinear interpolations and the bit scan are independent chains the
+    // scheduler overlaps; the batch-axis segments (batch 1 for the draft
+    // decode, gamma for the verify) and the grids' constants are hoisted.
+    DSD_HD void session_run(int64_t i) {
+        ReqRec& r = rec(i);
+        if (phase(r) == kPhDone) return;
+        const int32_t g = gamma_s;
+        const int32_t prompt = r.prompt, output = r.output, nb = r.nbits;
+        // the scenario's latency table: lat[c] = {draft decode of g tokens,
+        // verify of g tokens} at context c (status word 0: all below 2^28 us)
+        const int2* lat = S.o_slat >= 0 ? reinterpret_cast<const int2*>(W.spec_lat + S.o_slat + 2) : nullptr;
+        if (busy(1) || SV(v_qhead, 1) >= 0 || g > 63 || !lat || W.spec_lat[S.o_slat] != 0 ||
+            link_us >= kSpecLatMax || prompt + output >= W.spec_lat[S.o_slat + 1] || nb < 1) {
+            begin_with(i, Decision{false, gamma_s});  // outside the loop's steady state
+            return;
+        }
+        int64_t ext = next_arr < N ? next_arr_t : INT64_MAX;
+        if (heap_n > 0 && ht(0) < ext) ext = ht(0);
+        // times relative to the entry: 32-bit, below xr <= 2^30, and every
+        // step adds less than 2^28, so no sum overflows
+        const int64_t base = now;
+        const int32_t xr = ext - base < (1 << 30) ? static_cast<int32_t>(ext - base) : (1 << 30);
+        const int32_t lk = static_cast<int32_t>(link_us);
+        // the target's state cannot change inside the loop
+        const bool target_ok = !busy(0) && SV(v_qhead, 0) < 0 && flag(r, kTpd);
+        const uint64_t* bits = W.bits + static_cast<int64_t>(rep) * W.c.bw + r.bitoff;
+        const int32_t nwords = (nb + 63) >> 6;
+        int32_t tokens = r.tokens, cur = r.cursor, ng = r.ng, nc = r.nc, prop = r.prop, acc = r.acc, lcr = r.lcr;
+        int64_t first = r.first;
+        int64_t busy0 = get_busy(0);
+        wait_word();  // the activation's refill of the slot word has landed
+        // the acceptance words at the cursor and after it
+        uint64_t w0 = *slot_word();
+        uint64_t w1 = (cur >> 6) + 1 < nwords ? bits[(cur >> 6) + 1] : 0;
+        int32_t nr = 0;  // now - base
+        int32_t nw = 0;  // verifies dispatched (net_wait_count; their wait is 0)
+        uint32_t seq = seq_next;
+        int32_t t2 = 0;  // proposal arrival of the last iteration (verify enqueue time)
+        int2 l;
+        int a_acc, a_cons;
+        bool full;
+        for (;;) {
+            l = lat[prompt + tokens];
+            // consume_acceptance (engine.cpp:17-32) at the cursor: the run of
+            // trailing ones of the g bits there, capped at g (bit g forced)
+            if (cur + g <= nb) {
+                const int sh = cur & 63;
+                const uint64_t w = (w0 >> sh) | ((w1 << 1) << (63 - sh));
+#ifdef __CUDA_ARCH__
+                a_acc = __ffsll(static_cast<long long>(~w | (1ull << g))) - 1;
+#else
+                a_acc = __builtin_ctzll(~w | (1ull << g));
+#endif
+                a_cons = a_acc < g ? a_acc + 1 : g;
+            } else {  // the window wraps past the request's last bit
+                a_acc = 0;
+                a_cons = 0;
+                int32_t c = cur;
+                while (a_cons < g) {
+                    const uint64_t bb = (bits[c >> 6] >> (c & 63)) & 1u;
+                    c = c + 1 == nb ? 0 : c + 1;
+                    ++a_cons;
+                    if (bb) ++a_acc; else break;
+                }
+            }
+            // IterationStart -> draft done -> proposal -> verify done -> result
+            const int32_t t4 = nr + l.x + lk + l.y + lk;
+            full = target_ok && t4 < xr;
+            if (!full) break;
+            // the whole iteration is the replica's next five events
+            t2 = nr + l.x + lk;
+            nr = t4;
+            ++ng;
+            ++nw;
+            busy0 += l.y;
+            int32_t ncur = cur + a_cons;
+            ncur = ncur == nb ? 0 : ncur;
+            if ((ncur >> 6) != (cur >> 6)) {  // the cursor moved to another word
+                const int32_t wi = ncur >> 6;
+                w0 = wi == (cur >> 6) + 1 ? w1 : bits[wi];
+                w1 = wi + 1 < nwords ? bits[wi + 1] : 0;
+            }
+            cur = ncur;
+            lcr = a_acc + 1;
+            prop += a_cons;
+            acc += a_acc;
+            const int32_t remaining = output - tokens;
+            tokens += lcr < remaining ? lcr : remaining;
+            ++nc;
+            if (first < 0) first = base + nr;
+            seq += 4;
+            if (tokens >= output) break;
+            ++seq;  // IterationStart at now: scheduled, and the earliest event
+        }
+        // where the last iteration stopped: the first event that is not the
+        // replica's earliest is left pending (defer), the handlers before it ran
+        int stage = 5;   // 5: the request completed
+        int64_t te = 0;  // the pending event's time
+        if (!full) {
+            const int32_t t1 = nr + l.x;
+            const int32_t tp = t1 + lk;
+            const int32_t t3 = tp + l.y;
+            ++ng;  // begin_iteration ran
+            if (!(t1 < xr)) {
+                stage = 0;
+                te = base + t1;
+            } else if (!(tp < xr)) {
+                stage = 1;
+                te = base + tp;
+                nr = t1;
+                seq += 1;
+            } else if (!target_ok) {
+                stage = 2;
+                nr = tp;
+                seq += 2;
+            } else if (!(t3 < xr)) {
+                stage = 3;
+                te = base + t3;
+                t2 = tp;
+                nr = tp;
+                seq += 2;
+                ++nw;
+                busy0 += l.y;
+            } else {
+                stage = 4;
+                te = base + t3 + lk;
+                t2 = tp;
+                nr = t3;
+                seq += 3;
+                ++nw;
+                busy0 += l.y;
+                int32_t ncur = cur + a_cons;
+                ncur = ncur == nb ? 0 : ncur;
+                if ((ncur >> 6) != (cur >> 6)) w0 = bits[ncur >> 6];
+                cur = ncur;
+                lcr = a_acc + 1;
+                prop += a_cons;
+                acc += a_acc;
+            }
+        }
+        now = base + nr;
+        seq_next = seq;
+        // write-back: the record as the step-by-step handlers leave it
+        r.tokens = tokens;
+        r.cursor = cur;
+        r.ng = ng;
+        r.prop = prop;
+        r.acc = acc;
+        r.lcr = lcr;
+        r.first = first;
+        r.pgamma = g;
+        r.tok1 = g;
+        r.next[1] = -1;
+        *slot_word() = w0;
+        set_flag(r, kFused, false);
+        net_wait_count += nw;
+        set_busy(0, busy0);
+        // both legs of a single jitter-free link: the proposal leg once a
+        // draft decode finished, the result leg once a verify did
+        if (stage >= 1 || nc > r.nc) r.outd = lk;
+        if (stage >= 4 || nc > r.nc) r.backd = lk;
+        r.nc = nc;
+        r.op[1] = static_cast<uint8_t>(stage >= 3 ? (kOpVerify | 4u) : kOpDecode);
+        // the item's enqueue time: the verify's (the proposal arrival) from
+        // stage 3 on, else begin_iteration's (stage 2: enqueue() sets it)
+        r.enq[1] = stage >= 3 ? base + t2 : (stage == 1 ? base + (nr - l.x) : now);
+        switch (stage) {
+            case 0:  // the draft is running the decode
+                set_phase(r, kPhSpeculating);
+                SV(v_run, 1) = static_cast<int32_t>(2 * i + 1);
+                set_busy_flag(1, true);
+                defer(te, info(kEvComputeDone, 0, 1u));
+                break;
+            case 1:  // the proposal is on the wire
+                set_phase(r, kPhInFlightToTarget);
+                defer(te, info(kEvNetArrive, kMsgProposal, static_cast<uint32_t>(i)));
+                break;
+            case 2:  // the verify waits for the target: the general enqueue + dispatch
+                set_phase(r, kPhVerifying);
+                enqueue(0, i, 1, kOpVerify, g, true);
+                break;
+            case 3:  // the target is running the verify
+                set_phase(r, kPhVerifying);
+                SV(v_run, 0) = static_cast<int32_t>(2 * i + 1);
+                set_busy_flag(0, true);
+                defer(te, info(kEvComputeDone, 0, 0u));
+                break;
+            case 4:  // the result is on the wire
+                set_phase(r, kPhInFlightToDraft);
+                defer(te, info(kEvNetArrive, kMsgResult, static_cast<uint32_t>(i)));
+                break;
+            default:  // the request is complete
+                set_phase(r, kPhInFlightToDraft);
+                push_act(act(kActFinish, static_cast<uint32_t>(i)));
+                break;
         }
     }
 
@@ -1548,7 +1784,10 @@ struct Engine {
                 push_act(act(kActItem, static_cast<uint32_t>(head)));
             }
         } else if (opaque(k) == kActBegin) {
-            begin(arg >> 1, arg & 1u);
+            if (spec && W.session_fast && (arg & 1u))
+                session_run(arg >> 1);
+            else
+                begin(arg >> 1, arg & 1u);
         } else if (opaque(k) == kActNetProposal) {
             ReqRec& r = rec(arg);
             set_phase(r, kPhVerifying);

@@ -91,6 +91,9 @@ struct DevScenario {
     // trace (TRACE / TRACE_POISSON)
     int64_t tr_n;
     int64_t o_tr_prompt, o_tr_output, o_tr_arrival, o_tr_drafter, o_tr_bitoff, o_tr_bits, o_tr_order;
+    // specialised kernel: offset (int32 elements) of this scenario's session
+    // latency table in Workspace::spec_lat, or -1 (Engine::session_run)
+    int64_t o_slat;
 };
 
 // Per-batch capacities (max over the batch's scenarios).
@@ -200,6 +203,15 @@ struct Workspace {
     // ---- optional step profile (DSD_STEP_STATS=1): [2k] cycles, [2k+1] count
     // per step kind, [32] warp iterations, [33] warp cycles, [34] max iterations
     unsigned long long* step_stats;
+    // specialised kernel: run the active session's speculation loop directly
+    // (Engine::session_run); env DSD_SESSION_FAST=0 disables it
+    int32_t session_fast;
+    // session latency tables of the specialised kernel (built by k_spec_lat
+    // at prepare): per (draft decode grid, verify grid, gamma) a status word
+    // (0: every entry below 2^28 us), then for each context c in [0, n) the
+    // pair {draft decode of gamma tokens at (1, c), verify at (gamma, c)} in
+    // us - latency_us() of both queries, so looking one up is exact
+    const int32_t* spec_lat;
     // ---- records (optional) ----
     int32_t collect;
     int64_t* rep_seqbase;  // [n] offset into the sequence arena

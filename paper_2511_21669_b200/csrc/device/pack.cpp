@@ -101,6 +101,7 @@ void pack_batch_into(Packed& P, const dsd_scenario* sc, size_t ns, const dsd_rep
         const dsd_scenario& s = sc[k];
         DevScenario& d = ds[k];
         std::memset(&d, 0, sizeof(d));
+        d.o_slat = -1;  // set by Runtime::prepare for specialised batches
         // error-message prefix, built only when a check fails
         const auto where = [k] { return "scenario " + std::to_string(k) + ": "; };
         if (s.n_targets < 1) cfg_error(where() + "target pool must be non-empty");

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <map>
 #include <numeric>
+#include <tuple>
 #include <vector>
 
 #include "engine.cuh"
@@ -121,7 +122,7 @@ __device__ __forceinline__ uint32_t vote_kind(unsigned best) {
 // the specialised kernel needs ~100 registers: more resident blocks per SM
 // leave room for thin warps (placement_list) in one wave
 #ifndef DSD_SPEC_MIN_BLOCKS
-#define DSD_SPEC_MIN_BLOCKS 10
+#define DSD_SPEC_MIN_BLOCKS 8
 #endif
 // kSpec: the single-pair specialisation (Engine::spec; kSmem only).
 // kAwc: the batch has AWC scenarios (cooperative AWC scratch + serving); the
@@ -219,6 +220,28 @@ __global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_
     if (live) e.finish();
 }
 
+// Session latency tables of the specialised kernel (Workspace::spec_lat):
+// one block row per table (blockIdx.y), contexts across threads.  Entry c is
+// {grid_latency_us(draft decode grid, 1, c, g), grid_latency_us(verify
+// grid, g, c, 0)} - the very calls dispatch_single_draft / _target make - so
+// a lookup is exact; a table with an entry >= kSpecLatMax is marked unusable
+// in its status word (session_run then takes the step-by-step path).
+__global__ void k_spec_lat(const char* blob, const SpecLatJob* jobs, int32_t* lat) {
+    const SpecLatJob j = jobs[blockIdx.y];
+    int32_t* t = lat + j.base;
+    const DevGrid& gd = *reinterpret_cast<const DevGrid*>(blob + j.o_gd);
+    const DevGrid& gt = *reinterpret_cast<const DevGrid*>(blob + j.o_gt);
+    for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < j.n;
+         c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t a = grid_latency_us(blob, gd, 1, c, j.g1);
+        const int64_t b = grid_latency_us(blob, gt, j.g1, c, 0);
+        if (a >= kSpecLatMax || b >= kSpecLatMax) atomicOr(&t[0], 1);
+        t[2 + 2 * c] = static_cast<int32_t>(a);
+        t[3 + 2 * c] = static_cast<int32_t>(b);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) t[1] = j.n;
+}
+
 // Collects the replicas whose shared-memory heap (or the specialised
 // kernel's shorter action stack) overflowed.
 __global__ void k_collect_overflow(Workspace W, int32_t* list, int32_t* count) {
@@ -276,7 +299,7 @@ struct RuntimeImpl {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[4] = {};
-    DevBuf blob, scen, reps, arena, summary, fail, ltot, seqbase, seqg, seqc, rec, busy, ovf, probe;
+    DevBuf blob, scen, reps, arena, summary, fail, ltot, seqbase, seqg, seqc, rec, busy, ovf, probe, slat, sjobs;
     // shared-memory heap slots per replica for small topologies (0 = always
     // run the HBM variant; env DSD_SMEM_HEAP overrides, for tests)
     // 7: with 8 server fields x 2 servers and one session slot a warp needs
@@ -312,6 +335,7 @@ struct RuntimeImpl {
     int64_t launches = 0;
     int64_t h2d_bytes = 0, d2h_bytes = 0;
     bool spec_stack_limit1 = false;  // DSD_SPEC_STACK_LIMIT=1 (tests: force the HBM re-run)
+    bool session_fast = true;        // Engine::session_run in the specialised kernel (DSD_SESSION_FAST=0: off)
     bool smem_launch = false;
     void* pinned = nullptr;  // host_summaries() buffer (page-locked)
     size_t pinned_bytes = 0;  // the last launch ran the shared-memory variant (+ HBM re-run)
@@ -339,6 +363,7 @@ Runtime::Runtime(int device) : impl_(new RuntimeImpl) {
     if (const char* s = std::getenv("DSD_STEP_STATS")) impl_->step_stats = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_SPEC_STACK_LIMIT")) impl_->spec_stack_limit1 = std::atoi(s) == 1;
     if (const char* s = std::getenv("DSD_SPECIALIZE")) impl_->specialize = std::atoi(s) != 0;
+    if (const char* s = std::getenv("DSD_SESSION_FAST")) impl_->session_fast = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_PLACEMENT")) impl_->placement = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_SPREAD")) impl_->spread = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_SPREAD_MAX")) impl_->spread_max = std::atof(s);
@@ -447,6 +472,47 @@ static std::vector<int32_t> placement_list(const Packed& P, size_t n, int64_t wa
     return pl;
 }
 
+// Session latency tables for a specialised batch: one per distinct (draft
+// decode grid, verify grid, gamma), covering every context a request of the
+// scenarios can reach (prompt + output: the length caps of a synthetic
+// workload, the longest trace record otherwise); sets each scenario's o_slat
+// (-1: no table, the session loop stays off).  Returns the int32 elements.
+static int64_t spec_lat_jobs(Packed& P, std::vector<SpecLatJob>& jobs) {
+    std::map<std::tuple<int64_t, int64_t, int32_t>, size_t> key_job;
+    std::vector<size_t> job_of(P.scen.size(), SIZE_MAX);
+    for (size_t k = 0; k < P.scen.size(); ++k) {
+        DevScenario& d = P.scen[k];
+        d.o_slat = -1;
+        int64_t maxctx = 0;
+        if (d.workload == 0) {
+            maxctx = d.p_cap + d.o_cap;
+        } else {
+            const int64_t* tp = reinterpret_cast<const int64_t*>(P.blob.data() + d.o_tr_prompt);
+            const int64_t* to = reinterpret_cast<const int64_t*>(P.blob.data() + d.o_tr_output);
+            for (int64_t q = 0; q < d.tr_n; ++q) maxctx = std::max(maxctx, tp[q] + to[q]);
+        }
+        if (maxctx < 0 || maxctx >= (1 << 20) || d.gamma > 63) continue;  // no table
+        const int32_t* tg = reinterpret_cast<const int32_t*>(P.blob.data() + d.o_tgrid);
+        const int32_t* dg = reinterpret_cast<const int32_t*>(P.blob.data() + d.o_dgrid);
+        const int64_t o_gt = d.o_grids + static_cast<int64_t>(sizeof(DevGrid)) * tg[1];
+        const int64_t o_gd = d.o_grids + static_cast<int64_t>(sizeof(DevGrid)) * dg[1];
+        const int32_t g1 = std::max(1, d.gamma);
+        auto it = key_job.emplace(std::make_tuple(o_gd, o_gt, g1), jobs.size()).first;
+        if (it->second == jobs.size()) jobs.push_back(SpecLatJob{o_gd, o_gt, 0, g1, 0});
+        SpecLatJob& j = jobs[it->second];
+        j.n = std::max<int32_t>(j.n, static_cast<int32_t>(maxctx + 1));
+        job_of[k] = it->second;
+    }
+    int64_t off = 0;
+    for (SpecLatJob& j : jobs) {
+        j.base = off;
+        off += 2 + 2 * static_cast<int64_t>(j.n);
+    }
+    for (size_t k = 0; k < P.scen.size(); ++k)
+        if (job_of[k] != SIZE_MAX) P.scen[k].o_slat = jobs[job_of[k]].base;
+    return off;
+}
+
 void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n,
                       bool collect, bool feature_probe) {
     RuntimeImpl& R = *impl_;
@@ -468,6 +534,15 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
     pack_batch_into(P, sc, ns, reps, n, feature_probe);
     lap("pack");
     const Caps& c = P.caps;
+    // every scenario fits the single-pair specialisation (Engine::spec)
+    R.spec_ok = c.ns == 2;
+    for (const DevScenario& d : P.scen)
+        R.spec_ok = R.spec_ok && d.n_targets == 1 && d.n_drafts == 1 && !d.fused_everything && d.window_kind == 0 &&
+                    d.batching == 0 && d.batching_window_us == 0 && d.jitter_free && d.n_dg == 1 && d.n_tg == 1 &&
+                    !d.has_order && !d.pair_stats;
+    std::vector<SpecLatJob> jobs;
+    int64_t slat_elems = 0;
+    if (R.spec_ok && R.session_fast) slat_elems = spec_lat_jobs(P, jobs);
     // ---- upload blob, scenarios, replicas ----
     R.blob.ensure(P.blob.size());
     DSD_CUDA(cudaMemcpyAsync(R.blob.p, P.blob.data(), P.blob.size(), cudaMemcpyHostToDevice, R.stream));
@@ -511,17 +586,30 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
     W.summary = static_cast<DevSummary*>(R.summary.p);
     W.fail = static_cast<int32_t*>(R.fail.p);
     W.collect = collect ? 1 : 0;
+    W.session_fast = R.session_fast ? 1 : 0;
     if (feature_probe) {
         R.probe.ensure(sizeof(double) * kProbeFields * std::max<size_t>(n, 1));
         W.probe = static_cast<double*>(R.probe.p);
     }
+    // session latency tables (specialised batches)
+    W.spec_lat = nullptr;
+    if (slat_elems > 0) {
+        R.slat.ensure(sizeof(int32_t) * static_cast<size_t>(slat_elems));
+        R.sjobs.ensure(sizeof(SpecLatJob) * jobs.size());
+        DSD_CUDA(cudaMemsetAsync(R.slat.p, 0, sizeof(int32_t) * static_cast<size_t>(slat_elems), R.stream));
+        DSD_CUDA(cudaMemcpyAsync(R.sjobs.p, jobs.data(), sizeof(SpecLatJob) * jobs.size(), cudaMemcpyHostToDevice,
+                                 R.stream));
+        int32_t nmax = 0;
+        for (const SpecLatJob& j : jobs) nmax = std::max(nmax, j.n);
+        const dim3 g(static_cast<unsigned>(std::min<int64_t>(64, (nmax + 255) / 256)), static_cast<unsigned>(jobs.size()));
+        k_spec_lat<<<g, 256, 0, R.stream>>>(W.blob, static_cast<const SpecLatJob*>(R.sjobs.p),
+                                            static_cast<int32_t*>(R.slat.p));
+        DSD_CUDA(cudaGetLastError());
+        W.spec_lat = static_cast<const int32_t*>(R.slat.p);
+        R.h2d_bytes += static_cast<int64_t>(sizeof(SpecLatJob) * jobs.size());
+    }
     // lane placement
     R.place_n = 0;
-    R.spec_ok = c.ns == 2;
-    for (const DevScenario& d : P.scen)
-        R.spec_ok = R.spec_ok && d.n_targets == 1 && d.n_drafts == 1 && !d.fused_everything && d.window_kind == 0 &&
-                    d.batching == 0 && d.batching_window_us == 0 && d.jitter_free && d.n_dg == 1 && d.n_tg == 1 &&
-                    !d.has_order && !d.pair_stats;
     // the lane placement is computed by launch() while k_stage runs
     R.place_pending = true;
     R.n = n;
