@@ -189,6 +189,9 @@ __global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_
         const unsigned score = kind == kActNone ? 0u : vote_score(static_cast<unsigned>(__popc(peers)), kind);
         const unsigned best = __reduce_max_sync(0xffffffffu, score);
         if (best == 0u) break;
+        if constexpr (kStats) {  // warp rounds per selected kind (lanes per round = steps / rounds)
+            if ((threadIdx.x & (kLanes - 1)) == 0) atomicAdd(&W.step_stats[40 + vote_kind(best)], 1ull);
+        }
         if (kind == vote_kind(best)) {
             // the selected lanes run their continuation chain up to the next
             // barrier kind (kBarrierKinds)
@@ -804,6 +807,7 @@ void Runtime::sync() {
     }
     if (R.step_stats && R.W.step_stats) {
         unsigned long long s[64];
+        static_assert(40 + kActKinds <= 64, "step stats layout");
         DSD_CUDA(cudaMemcpy(s, R.stats.p, sizeof(s), cudaMemcpyDeviceToHost));
         static const char* names[] = {"pop", "arrival", "net_prompt", "net_proposal", "net_result", "begin",
                                       "compute_done", "item", "finish", "activate", "dispatch", "send_prompt"};
@@ -813,8 +817,9 @@ void Runtime::sync() {
                      s[32], s[34], s[33], steps);
         for (int k = 0; k < kActKinds; ++k)
             if (s[2 * k + 1])
-                std::fprintf(stderr, "  %-13s steps %12llu  avg cycles/step %8.1f\n", names[k], s[2 * k + 1],
-                             static_cast<double>(s[2 * k]) / static_cast<double>(s[2 * k + 1]));
+                std::fprintf(stderr, "  %-13s steps %12llu  avg cycles/step %8.1f  rounds %10llu  lanes/round %5.2f\n",
+                             names[k], s[2 * k + 1], static_cast<double>(s[2 * k]) / static_cast<double>(s[2 * k + 1]),
+                             s[40 + k], s[40 + k] ? static_cast<double>(s[2 * k + 1]) / s[40 + k] : 0.0);
     }
 }
 
