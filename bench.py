@@ -1,17 +1,29 @@
 #!/usr/bin/env python3
-"""Benchmark: simulated events/s on the 65,536-replica DSD sweep (BASELINE.json
-configs[4]) on N B200s.
+"""Benchmark: simulated events/s of the DSD-Sim simulate-a-sweep path on N B200s.
 
-One "step" = one pass of the sweep's simulate path over all replicas of this
-rank's shard: the device workload-staging kernel (generate_synthetic for every
-replica) + the discrete-event simulation kernel, and for N > 1 the NCCL
-all-gather of per-replica summaries.  `value` is timed with CUDA events on the
-library's stream with inputs resident in HBM (L2 flushed between steps by a
-512 MiB memset that is outside the timed events); `e2e` is the same metric
-through the public C ABI with host buffers (YAML parse, sweep planning,
-host->device upload, kernels, device->host summaries, per-point means).
+Default workload: BASELINE.json configs[4], the 65,536-replica C5 sweep
+(SURVEY.md §8(d)): 4,096 points (gamma 1..16 x rtt 2..32 ms x alpha 0.50..0.95)
+x 16 repetitions of the C1 single edge-cloud pair.
+
+One "step" = one pass of the sweep's simulate path over this rank's replicas:
+the device workload-staging kernel (generate_synthetic for every replica) +
+the discrete-event simulation kernel, and for N > 1 the NCCL all-gather of the
+96-byte per-replica summaries.  Scaling is STRONG by default: the same 65,536
+replicas are dealt across the N GPUs in cost order (the split the library's
+multi-device handle makes); --weak gives every GPU its own 65,536 replicas.
+
+  value  CUDA events on the library's stream, inputs resident in HBM, L2
+         flushed between steps (512 MiB memset outside the timed events),
+         max over ranks.
+  e2e    the same metric through the public C ABI with host buffers:
+         dsd_run_sweep (YAML parse, sweep planning, pack + H2D, kernels, D2H
+         of the summaries, per-point means, summary JSON/CSV).  For N > 1 rank
+         0 makes the drop-in call on a handle over all N GPUs
+         (dsd_create_devices) while the other ranks wait.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--weak] [--workload c5|c2_seeds|c3_seeds|c4s_seeds|c4a_seeds|
+                   c1_single|c2_single|c3_single|c4s_single|c4a_single]
 """
 import argparse
 import json
@@ -24,20 +36,52 @@ import time
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
-SPEC = os.path.join(REPO, "configs", "c5_sweep_65536.yaml")
-SPEC_DIR = os.path.dirname(SPEC)
-
-
-def sweep_text(world):
-    """The C5 sweep with 16*world repetitions: every rank simulates its own
-    65,536-replica shard (repetitions r, r+world, ...) of one sweep (weak scaling)."""
-    text = open(SPEC).read()
-    assert "repetitions: 16" in text
-    return text.replace("repetitions: 16", f"repetitions: {16 * world}")
+CONFIGS = os.path.join(REPO, "configs")
+GOLDEN = os.path.join(REPO, "tests", "golden", "configs")
+GEN = os.path.join(REPO, "tests", "golden", "_gen")  # mixed.jsonl / model.json (reference-built fixtures)
 B_EV = 64  # algorithmic replica-state bytes per simulated event (SURVEY §8(d))
 METRIC = "simulated_events_per_sec"
-WORKLOAD = ("c5_sweep_65536: 4096 points (gamma 1..16 x rtt 2..32 ms x alpha 0.50..0.95) x 16 reps per GPU "
-            "(16*N repetitions sharded by repetition over N GPUs), C1 single edge-cloud pair")
+C5 = os.path.join(CONFIGS, "c5_sweep_65536.yaml")
+
+
+def _seed_sweep(base, reps, n_points):
+    """n_points x reps replicas of one config: the points differ only in the
+    default link RTT (network.rtt_ms 2..n_points+1; every C3/C4 pair has an
+    override, so there it only changes the point id and hence the seeds) -
+    the reference's run_sweep parallelises over points, not repetitions."""
+    vals = ", ".join(str(v) for v in range(2, n_points + 2))
+    return f"base: {base}\nseed: 42\nrepetitions: {reps}\naxes:\n  network.rtt_ms: [{vals}]\n"
+
+
+# name -> (kind, text or path, base_dir, description)
+WORKLOADS = {
+    "c5": ("sweep", C5, CONFIGS,
+           "c5_sweep_65536: 4096 points (gamma 1..16 x rtt 2..32 ms x alpha 0.50..0.95) x 16 reps, "
+           "C1 single edge-cloud pair (BASELINE configs[4])"),
+    "c2_seeds": ("sweep", _seed_sweep(os.path.join(GOLDEN, "c2_8x1_batching.yaml"), 32, 32),
+                 GOLDEN, "C2 (8 drafts x 1 target, 2 ms batching window, jsq): rtt 2..33 ms x 32 seeds = 1024 replicas"),
+    "c3_seeds": ("sweep", _seed_sweep(os.path.join(GOLDEN, "c3_64x4_awc.yaml"), 16, 16), GEN,
+                 "C3 (64 drafts x 4 targets, heterogeneous RTT, AWC) x 256 seeds"),
+    "c4s_seeds": ("sweep", _seed_sweep(os.path.join(GOLDEN, "c4_1024x16_static.yaml"), 4, 16), GEN,
+                  "C4 static (1024 drafts x 16 targets, mixed trace) x 64 seeds"),
+    "c4a_seeds": ("sweep", _seed_sweep(os.path.join(GOLDEN, "c4_1024x16_awc.yaml"), 4, 16), GEN,
+                  "C4 AWC (1024 drafts x 16 targets, mixed trace) x 64 seeds"),
+    "c1_single": ("single", os.path.join(GOLDEN, "c1_single_pair.yaml"), GOLDEN, "C1 single run"),
+    "c2_single": ("single", os.path.join(GOLDEN, "c2_8x1_batching.yaml"), GOLDEN, "C2 single run"),
+    "c3_single": ("single", os.path.join(GOLDEN, "c3_64x4_awc.yaml"), GEN, "C3 single run (AWC)"),
+    "c4s_single": ("single", os.path.join(GOLDEN, "c4_1024x16_static.yaml"), GEN, "C4 static single run"),
+    "c4a_single": ("single", os.path.join(GOLDEN, "c4_1024x16_awc.yaml"), GEN, "C4 AWC single run"),
+}
+
+
+def workload_text(name, weak_world=1):
+    kind, src, base, desc = WORKLOADS[name]
+    text = open(src).read() if os.path.exists(src) else src
+    if kind == "sweep" and weak_world > 1:
+        import re
+        m = re.search(r"repetitions: (\d+)", text)
+        text = text.replace(m.group(0), f"repetitions: {int(m.group(1)) * weak_world}")
+    return kind, text, base, desc
 
 
 def env_int(k, d):
@@ -57,18 +101,23 @@ def peaks():
 
 
 def ncu_summary():
-    """The committed ncu --set full summary of the simulate kernel (profiles/), if any."""
-    p = os.path.join(REPO, "profiles", "ncu_sim_kernel.json")
+    """The committed ncu --set full summary of the simulate kernel on the
+    default workload at N=1 (profiles/ncu_sim_kernel.json), if any."""
     try:
-        with open(p) as f:
+        with open(os.path.join(REPO, "profiles", "ncu_sim_kernel.json")) as f:
             return json.load(f)
     except Exception:
         return {}
 
 
-def ncu_traffic():
-    """dram read+write bytes per simulate-kernel launch from the committed ncu capture, if any."""
-    return ncu_summary().get("dram_bytes_per_launch")
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 class Clocks:
@@ -117,24 +166,30 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference arm: the reference simulator (oracle/_ref) on host cores
+# CPU reference: the reference simulator (oracle/_ref) on the host cores
 # ---------------------------------------------------------------------------
-def cpu_reference(seconds_target=8.0, threads=None):
-    """Times the reference's own run_sweep worker (resolve_config + run_simulation
-    + aggregate_run per replica, sweep.cpp:112-150) on a strided sample of the
-    sweep's points with all host threads.  Falls back to the C restatement
-    (kind "port") when oracle/_ref was not built."""
+def cpu_reference(name, threads=None, sample_points=None):
+    """Times the reference's own run_sweep worker (resolve_config +
+    run_simulation + aggregate_run per replica, sweep.cpp:112-150) over the
+    WHOLE sweep (every point x every repetition) with all host threads, or the
+    reference's run_simulation of a single config on one core.  Falls back to
+    the C restatement (kind "port") when oracle/_ref was not built."""
     sys.path.insert(0, os.path.join(REPO, "tests"))
     threads = threads or os.cpu_count() or 1
-    spec = open(SPEC).read()
-    base = os.path.dirname(SPEC)
+    kind, text, base, desc = workload_text(name)
     import reforacle
+    if kind == "single":
+        if not reforacle.available():
+            raise SystemExit("reference oracle not built")
+        t = time.perf_counter()
+        _, ev, _, _ = reforacle.run_config(text, base)
+        dt = time.perf_counter() - t
+        return {"events": float(ev), "replicas": 1.0, "seconds": dt, "kind": "reference", "cores": 1,
+                "sample": f"{desc}: the whole run ({ev} events) on one core (a run is single-threaded)"}
     if reforacle.available():
-        def run(npts):
-            pts = [int(i * 4096 / npts) for i in range(npts)]
-            r = reforacle.sweep_bench(spec, base, threads, pts)
-            return r["events"], r["replicas"], r["seconds"]
-        kind = "reference"
+        r = reforacle.sweep_bench(text, base, threads, sample_points)
+        ev, rep, sec = r["events"], r["replicas"], r["seconds"]
+        k = "reference"
     else:
         import ctypes
         import restate
@@ -142,38 +197,32 @@ def cpu_reference(seconds_target=8.0, threads=None):
         L = _lib.lib()
         p = ctypes.c_void_p()
         err = ctypes.create_string_buffer(1024)
-        assert L.dsd_plan_sweep(spec.encode(), base.encode(), 0, 1, ctypes.byref(p), err, 1024) == 0
+        assert L.dsd_plan_sweep(text.encode(), base.encode(), 0, 1, ctypes.byref(p), err, 1024) == 0
         sc, rp = ctypes.c_void_p(), ctypes.c_void_p()
         L.dsd_sweep_plan_scenarios(p, ctypes.byref(sc))
         nrep = L.dsd_sweep_plan_replicas(p, ctypes.byref(rp))
-        reps = ctypes.cast(rp, ctypes.POINTER(restate.Replica))
-
-        def run(npts):
-            idx = [int(i * nrep / (npts * 16)) for i in range(npts * 16)]
-            arr = (restate.Replica * len(idx))(*[reps[i] for i in idx])
-            out = (_lib.ReplicaSummary * len(idx))()
-            t = time.perf_counter()
-            restate.olib().oracle_run_batch(sc, arr, len(idx), threads, out, err, 1024)
-            dt = time.perf_counter() - t
-            return float(sum(o.events_processed for o in out)), float(len(idx)), dt
-        kind = "port"
-    ev, rep, sec = run(max(8, threads))  # calibration probe
-    rate = rep / max(sec, 1e-6)
-    npts = int(min(4096, max(16, rate * seconds_target / 16)))
-    ev, rep, sec = run(npts)
-    return {"events": ev, "replicas": rep, "seconds": sec, "kind": kind, "cores": threads,
-            "sample": f"{npts} of 4096 sweep points (strided) x 16 reps = {int(rep)} replicas, {int(ev)} events"}
+        out = (_lib.ReplicaSummary * nrep)()
+        t = time.perf_counter()
+        restate.olib().oracle_run_batch(sc, rp, nrep, threads, out, err, 1024)
+        sec = time.perf_counter() - t
+        ev, rep, k = float(sum(o.events_processed for o in out)), float(nrep), "port"
+    what = "the whole sweep" if not sample_points else f"{len(sample_points)} points of the sweep"
+    return {"events": ev, "replicas": rep, "seconds": sec, "kind": k, "cores": threads,
+            "sample": f"{desc}: {what} ({int(rep)} replicas, {int(ev)} events) on {threads} threads "
+                      f"({cpu_model()})"}
 
 
 def main_reference(args, rank, world):
     if rank != 0:
         return
+    kind = WORKLOADS[args.workload][0]
+    # warm-up: a few points (threads, allocator, page cache) - not the full sweep
     for _ in range(args.warmup):
-        cpu_reference(seconds_target=2.0)
+        cpu_reference(args.workload, sample_points=list(range(0, 4096, 256)) if kind == "sweep" else None)
     ev = rep = sec = 0.0
     last = None
     for _ in range(args.steps):
-        r = cpu_reference(seconds_target=6.0)
+        r = cpu_reference(args.workload)
         ev += r["events"]
         rep += r["replicas"]
         sec += r["seconds"]
@@ -182,9 +231,10 @@ def main_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * sec / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
-        "data": "synthetic (reference generate_synthetic streams)",
-        "config": {"workload": WORKLOAD, "replicas_sampled_per_step": last["replicas"] if last else 0},
+        "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
+        "dtype": "int64+f64", "data": "synthetic (reference generate_synthetic streams)",
+        "config": {"workload": WORKLOADS[args.workload][3], "replicas_per_step": int(last["replicas"]),
+                   "events_per_step": int(last["events"])},
         "replicas_per_sec": rep / sec,
         "cpu_baseline": {"value": value, "unit": "events/s", "cores": last["cores"], "kind": last["kind"],
                          "sample": last["sample"]},
@@ -196,26 +246,95 @@ def main_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def roofline(ev_local, sim_ms, clk):
+    peak, peak_kind = peaks()
+    achieved = B_EV * ev_local / (sim_ms / 1e3) / 1e9
+    nc = ncu_summary()
+    out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+           "traffic": nc.get("dram_bytes_per_launch"), "peak_source": peak_kind, "bytes_per_event": B_EV,
+           "kernel": "k_simulate", "kernel_ms": sim_ms,
+           "from_committed_capture": ["traffic", "issue.warp_instructions", "issue.threads_per_instruction",
+                                      "ncu_issue_active_pct", "ncu_stall_pct"]}
+    # The DES is latency/issue-bound, not HBM-bound: the issue
+    # roofline = warp instructions of the launch (deterministic for the
+    # workload; from the committed capture) / (SMs x 4 schedulers x clock x
+    # the live kernel time), and the SIMT efficiency of those instructions.
+    wi = nc.get("warp_instructions")
+    if wi and clk and clk.get("sm_mhz"):
+        sms = nc.get("sms", 148)
+        slots = sms * 4 * clk["sm_mhz"] * 1e6 * (sim_ms / 1e3)
+        out["issue"] = {"warp_instructions": wi, "issue_slots": slots, "frac": wi / slots,
+                        "threads_per_instruction": nc.get("threads_per_instruction"),
+                        "clock_mhz": clk["sm_mhz"], "sms": sms}
+    out["ncu_issue_active_pct"] = nc.get("issue_active_pct")
+    out["ncu_stall_pct"] = dict(list(nc.get("stall_pct", {}).items())[:4])
+    return out
+
+
+def main_single(args, rank, world, local_rank):
+    """A single config through dsd_run_simulation (one replica; no sharding)."""
+    import torch
+    from paper_2511_21669_b200 import Simulator
+    if rank != 0:
+        return
+    _, text, base, desc = workload_text(args.workload)
+    torch.cuda.set_device(local_rank)
+    sim = Simulator(local_rank)
+    for _ in range(args.warmup):
+        out = sim.run_simulation(text, base_dir=base, report=False)
+    clocks = Clocks([local_rank])
+    dev_ms, wall = [], []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        out = sim.run_simulation(text, base_dir=base, report=False)
+        wall.append(time.perf_counter() - t)
+        dev_ms.append(sim.last_kernel_ms()["total_ms"])
+    clk = clocks.stop()
+    ev = out.events_processed
+    ms = sum(dev_ms) / len(dev_ms)
+    e2e_s = sum(wall) / len(wall)
+    h2d, d2h = sim.last_transfer_bytes()
+    line = {"metric": METRIC, "value": ev / (ms / 1e3), "unit": "events/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "none",
+            "vs_baseline": None, "dtype": "int64+f64", "data": "synthetic / reference-built trace fixtures",
+            "config": {"workload": desc, "events_per_step": ev, "replicas": 1},
+            "e2e": {"value": ev / e2e_s, "unit": "events/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_s, "path": "dsd_run_simulation"},
+            "gpu_launches": sim.last_launch_count() * args.steps}
+    if clk:
+        line["clocks"] = clk
+    if not args.no_cpu_baseline:
+        cb = cpu_reference(args.workload)
+        line["cpu_baseline"] = {"value": cb["events"] / cb["seconds"], "unit": "events/s", "cores": cb["cores"],
+                                "kind": cb["kind"], "sample": cb["sample"]}
+    print(json.dumps(line), flush=True)
+
+
 def main_ours(args, rank, world, local_rank):
-    import numpy as np
     import torch
     from paper_2511_21669_b200 import Simulator
 
+    if WORKLOADS[args.workload][0] == "single":
+        return main_single(args, rank, world, local_rank)
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     sim = Simulator(local_rank)
-    spec = sweep_text(world)
-    n_rep, n_pts = sim.prepare_sweep(spec, base_dir=SPEC_DIR, shard=rank, n_shards=world)
+    _, spec, base, desc = workload_text(args.workload, world if args.weak else 1)
+    # this rank's shard: strong = 1/N of the same replicas, weak = 1/N of an N-times larger sweep
+    n_rep, n_pts = sim.prepare_sweep(spec, base_dir=base, shard=rank, n_shards=world)
     stream = torch.cuda.ExternalStream(sim.stream(), device=torch.device("cuda", local_rank))
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     sum_ptr, sum_bytes = sim.device_summaries()
     gather = None
     if world > 1:
-        # per-replica summaries, gathered once per step over NVLink
-        max_rep = n_rep
+        # per-replica summaries, gathered once per step over NVLink (SURVEY §8(e));
+        # shards differ by at most one replica: pad to the largest
+        nmax = torch.tensor([n_rep], dtype=torch.int64, device="cuda")
+        dist.all_reduce(nmax, op=dist.ReduceOp.MAX)
+        max_rep = int(nmax.item())
         rows = torch.zeros(max_rep * 96, dtype=torch.uint8, device="cuda")
         gather = torch.zeros(world * max_rep * 96, dtype=torch.uint8, device="cuda")
 
@@ -271,70 +390,59 @@ def main_ours(args, rank, world, local_rank):
         ev_all, rep_all = ev_local, float(n_rep)
     ms_per_step = tot_ms / args.steps
     value = ev_all / (ms_per_step / 1e3)
-
-    # ---- e2e through the public C ABI with host buffers ----
-    e2e_times = []
-    h2d = d2h = 0
-    for k in range(args.steps + 1):
-        if dist:
-            dist.barrier()
-        t = time.perf_counter()
-        if world == 1:
-            out = sim.run_sweep(spec, base_dir=SPEC_DIR)
-            assert out.failed_points == 0
-        else:
-            sim.prepare_sweep(spec, base_dir=SPEC_DIR, shard=rank, n_shards=world)
-            sim.launch()
-            s2 = sim.summaries()
-            _ = s2["throughput_rps"].sum()
-        dt = time.perf_counter() - t
-        if k > 0:  # first call warms the host caches
-            e2e_times.append(dt)
-        h2d, d2h = sim.last_transfer_bytes()
-    e2e_s = sum(e2e_times) / len(e2e_times)
-    if dist:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    # restore the prepared device batch
-    if world == 1:
-        sim.prepare_sweep(spec, base_dir=SPEC_DIR, shard=rank, n_shards=world)
-
-    if rank != 0:
-        if dist:
-            dist.destroy_process_group()
-        return
-    peak, peak_kind = peaks()
     sim_avg = sum(sim_ms) / len(sim_ms)
-    achieved = B_EV * ev_local / (sim_avg / 1e3) / 1e9
-    traffic = ncu_traffic()
+    launches = sim.last_launch_count() * args.steps
+
+    # ---- e2e through the public C ABI with host buffers: the drop-in call ----
+    e2e_s, h2d, d2h, e2e_path = None, 0, 0, "dsd_run_sweep"
+    if dist:
+        dist.barrier()
+    if rank == 0:
+        devices = list(range(world))
+        esim = sim if world == 1 else Simulator(devices)
+        if world > 1:
+            e2e_path = f"dsd_run_sweep on dsd_create_devices({devices}) from rank 0"
+        times = []
+        for k in range(args.steps + 1):
+            t = time.perf_counter()
+            out = esim.run_sweep(spec, base_dir=base)
+            dt = time.perf_counter() - t
+            assert out.failed_points == 0
+            if k > 0:  # the first call warms the host caches and the other devices
+                times.append(dt)
+            h2d, d2h = esim.last_transfer_bytes()
+        e2e_s = sum(times) / len(times)
+        e2e_events = out.events_processed
+        if esim is not sim:
+            esim.close()
+    if dist:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
     line = {
         "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int64+f64",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "int64+f64",
         "data": "synthetic (reference generate_synthetic streams, regenerated on device every step)",
-        "config": {"workload": WORKLOAD, "replicas": int(rep_all), "points": n_pts,
-                   "events_per_step": int(ev_all), "l2": "flushed between steps (512 MiB memset)",
-                   "parallelism": f"replica shards x{world} + NCCL all-gather of summaries" if world > 1
-                   else "single GPU"},
+        "config": {"workload": desc, "replicas": int(rep_all), "points": n_pts, "events_per_step": int(ev_all),
+                   "l2": "flushed between steps (512 MiB memset)",
+                   "parallelism": (f"{'weak' if args.weak else 'strong'}: replicas dealt over {world} GPUs in "
+                                   f"cost order + NCCL all-gather of summaries") if world > 1 else "single GPU"},
         "replicas_per_sec": rep_all / (ms_per_step / 1e3),
-        "e2e": {"value": ev_all / e2e_s, "unit": "events/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_s,
-                "path": "dsd_run_sweep" if world == 1 else "dsd_prepare_sweep+dsd_batch_launch+dsd_batch_summaries"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_kind, "bytes_per_event": B_EV,
-                     "kernel": "k_simulate", "kernel_ms": sim_avg,
-                     # the DES is latency-bound, not HBM-bound: the
-                     # committed capture's SM issue activity and top warp stalls
-                     "ncu_issue_active_pct": ncu_summary().get("issue_active_pct"),
-                     "ncu_stall_pct": dict(list(ncu_summary().get("stall_pct", {}).items())[:4])},
-        "gpu_launches": sim.last_launch_count() * args.steps,
+        "e2e": {"value": e2e_events / e2e_s, "unit": "events/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_s, "path": e2e_path},
+        "roofline": roofline(ev_local, sim_avg, clk),
+        "gpu_launches": launches,
         "wall_s": wall,
     }
+    if world > 1:
+        line["rank0"] = {"replicas": n_rep, "events": int(ev_local), "sim_kernel_ms": sim_avg}
     if clk:
         line["clocks"] = clk
     if world == 1 and not args.no_cpu_baseline:
-        cb = cpu_reference()
+        cb = cpu_reference(args.workload)
         line["cpu_baseline"] = {"value": cb["events"] / cb["seconds"], "unit": "events/s", "cores": cb["cores"],
                                 "kind": cb["kind"], "sample": cb["sample"],
                                 "replicas_per_sec": cb["replicas"] / cb["seconds"]}
@@ -356,6 +464,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
+    ap.add_argument("--weak", action="store_true", help="every GPU simulates its own copy of the workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

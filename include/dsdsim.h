@@ -30,9 +30,14 @@
  *     config / validation / unknown profile key / corrupt model), DSD_ERR_RUNTIME.
  *     A human-readable message with the reference's error text is written to
  *     err[0..errlen).
- *   - A handle drives exactly one CUDA device and must be used from one host
- *     thread at a time (the reference Engine is single-threaded too,
- *     SPEC.md:76).  Multi-GPU runs create one handle per device/process.
+ *   - A handle drives one or more CUDA devices (dsd_create_devices) and must
+ *     be used from one host thread at a time (the reference Engine is
+ *     single-threaded too).  The replicas of every batch / sweep
+ *     are dealt across the handle's devices in cost order and run
+ *     concurrently, one stream per device; results always come back in the
+ *     caller's replica order, identical to a one-device run.  (One process
+ *     per GPU, each with a one-device handle and dsd_prepare_sweep's shards,
+ *     is the other way to use several GPUs.)
  *     Internally the sweep planning and summary loops run on a process-wide
  *     pool of host worker threads (DSD_HOST_THREADS), and dsd_run_sweep frees
  *     its host batch on a helper thread that the next call or dsd_destroy
@@ -208,9 +213,16 @@ typedef struct dsd_request_record {
 
 typedef struct dsd_handle dsd_handle;
 
-/* Library / device management. */
+/* Library / device management.  dsd_create(d) == dsd_create_devices(&d, 1).
+ * dsd_create_devices replaces run_sweep's `parallelism` worker pool
+ * (proj/src/runner/sweep.cpp:109-160) with a list of GPUs: every entry point
+ * that takes the handle spreads its replicas over all of them. */
 int dsd_abi_version(void);
 int dsd_create(int device_ordinal, dsd_handle** out, char* err, size_t errlen);
+int dsd_create_devices(const int* device_ordinals, int n_devices, dsd_handle** out, char* err, size_t errlen);
+int dsd_device_count(dsd_handle* h);
+/* Replicas of the prepared batch on each device (returns the device count). */
+int dsd_batch_shard_sizes(dsd_handle* h, int64_t* sizes, int cap);
 void dsd_destroy(dsd_handle* h);
 
 /* Runs n replicas of the given scenarios on the handle's GPU (one Engine run
@@ -241,7 +253,8 @@ int dsd_batch_sync(dsd_handle* h, char* err, size_t errlen);
 int dsd_batch_summaries(dsd_handle* h, dsd_replica_summary* summaries, size_t n, char* err,
                         size_t errlen);
 /* Device pointer + byte size of the summary array of the prepared batch
- * (valid until the next prepare/destroy); lets a caller gather it with NCCL. */
+ * (valid until the next prepare/destroy); lets a caller gather it with NCCL.
+ * One-device handles only. */
 int dsd_batch_device_summaries(dsd_handle* h, void** dev_ptr, size_t* bytes);
 /* cudaStream_t of the handle, as an opaque pointer (for event timing). */
 void* dsd_stream(dsd_handle* h);
@@ -274,11 +287,14 @@ int dsd_run_sweep(dsd_handle* h, const char* sweep_yaml, const char* base_dir,
                   const char* out_dir, char** summary_json, char** summary_csv,
                   double* totals, char* err, size_t errlen);
 
-/* Resolves a sweep spec into scenarios+replicas and prepares it on the device
- * (dsd_batch_prepare) without running it; returns replica count.  With
- * n_shards > 1 only the replicas g with g % n_shards == shard (point-major,
- * repetition-minor order) are kept, i.e. one GPU's share of the sweep.  Used
- * by the benchmark to time the kernels with inputs resident in HBM. */
+/* Resolves a sweep spec into scenarios+replicas and prepares it on the
+ * handle's device(s) (dsd_batch_prepare) without running it; returns the
+ * replica count.  With n_shards > 1 only shard `shard` of the replicas is
+ * kept - the cost-ordered deal dsd_create_devices makes (shard_of_replicas:
+ * replicas by decreasing estimated cost, dealt 0..N-1, N-1..0, ...), in
+ * point-major order - i.e. one GPU's share of the sweep when each GPU has
+ * its own process.  Used by the benchmark to time the kernels with inputs
+ * resident in HBM. */
 int dsd_prepare_sweep(dsd_handle* h, const char* sweep_yaml, const char* base_dir, int shard,
                       int n_shards, int64_t* n_replicas, int64_t* n_points, char* err,
                       size_t errlen);
@@ -298,8 +314,8 @@ void dsd_resolved_free(dsd_resolved* r);
 
 /* Resolves a sweep spec into scenarios + replicas without running it (the
  * object owns the arrays).  Replicas are point-major, repetition-minor; with
- * n_shards > 1 only replicas g with g % n_shards == shard are kept, exactly
- * the set dsd_prepare_sweep(shard, n_shards) runs.  dsd_sweep_plan_origin
+ * n_shards > 1 only the shard's replicas are kept (the cost-ordered deal),
+ * exactly the set dsd_prepare_sweep(shard, n_shards) runs.  dsd_sweep_plan_origin
  * returns, per kept replica, its (point index, repetition). */
 typedef struct dsd_sweep_plan dsd_sweep_plan;
 int dsd_plan_sweep(const char* sweep_yaml, const char* base_dir, int shard, int n_shards,

@@ -249,6 +249,10 @@ std::uint64_t ref_sweep_point_seed(std::uint64_t base, const char* point_id, int
     return sweep_point_seed(base, point_id, rep);
 }
 
+static int sweep_worker_run(const char* sweep_yaml, const char* base_dir, int threads,
+                            const std::int64_t* points, std::int64_t n_points, double* out, double* rows,
+                            char* err, std::size_t errlen);
+
 // Timing harness for the CPU baseline: the run_sweep worker (sweep.cpp:112-150)
 // reproduced with event counting (run_sweep itself does not return
 // RunResult::events_processed).  Runs the listed point indices (all when
@@ -258,6 +262,22 @@ std::uint64_t ref_sweep_point_seed(std::uint64_t base, const char* point_id, int
 int ref_sweep_bench(const char* sweep_yaml, const char* base_dir, int threads,
                     const std::int64_t* points, std::int64_t n_points, double* out, char* err,
                     std::size_t errlen) {
+    return sweep_worker_run(sweep_yaml, base_dir, threads, points, n_points, out, nullptr, err, errlen);
+}
+
+// The same worker over every point, keeping each replica's result: rows
+// [point * repetitions + rep][6] = {events_processed, end_time, completed,
+// throughput_rps, mean_ttft_ms, mean_tpot_ms} (RunResult, engine.hpp:44-53;
+// RunAggregates, runner.hpp:53-60).  A failed point's rows are all -1.
+int ref_sweep_replicas(const char* sweep_yaml, const char* base_dir, int threads, double* rows, char* err,
+                       std::size_t errlen) {
+    double out[4];
+    return sweep_worker_run(sweep_yaml, base_dir, threads, nullptr, 0, out, rows, err, errlen);
+}
+
+static int sweep_worker_run(const char* sweep_yaml, const char* base_dir, int threads,
+                            const std::int64_t* points, std::int64_t n_points, double* out, double* rows,
+                            char* err, std::size_t errlen) {
     return guarded(err, errlen, [&] {
         yaml::Node node = yaml::parse_string(sweep_yaml);
         SweepSpec spec = SweepSpec::from_node(node, base_dir ? base_dir : ".");
@@ -316,11 +336,24 @@ int ref_sweep_bench(const char* sweep_yaml, const char* base_dir, int threads,
                         tpot += agg.mean_tpot_ms;
                         events.fetch_add(o.result.events_processed);
                         replicas.fetch_add(1);
+                        if (rows) {
+                            double* row = rows + (idx * static_cast<std::size_t>(spec.repetitions) + rep) * 6;
+                            row[0] = static_cast<double>(o.result.events_processed);
+                            row[1] = static_cast<double>(o.result.end_time);
+                            row[2] = static_cast<double>(agg.completed);
+                            row[3] = agg.throughput_rps;
+                            row[4] = agg.mean_ttft_ms;
+                            row[5] = agg.mean_tpot_ms;
+                        }
                     }
                     volatile double sink = thr + ttft + tpot;
                     (void)sink;
                 } catch (const std::exception&) {
                     failed.fetch_add(1);
+                    if (rows)
+                        for (int rep = 0; rep < spec.repetitions; ++rep)
+                            for (int f = 0; f < 6; ++f)
+                                rows[(idx * static_cast<std::size_t>(spec.repetitions) + rep) * 6 + f] = -1.0;
                 }
             }
         };

@@ -53,7 +53,8 @@ class RequestRecord(ctypes.Structure):
 
 # Every symbol include/dsdsim.h declares (checked by tests/test_capi.py).
 EXPORTS = [
-    "dsd_abi_version", "dsd_create", "dsd_destroy", "dsd_run_batch", "dsd_fetch_records",
+    "dsd_abi_version", "dsd_create", "dsd_create_devices", "dsd_device_count", "dsd_batch_shard_sizes",
+    "dsd_destroy", "dsd_run_batch", "dsd_fetch_records",
     "dsd_batch_prepare", "dsd_batch_launch", "dsd_batch_sync", "dsd_batch_summaries",
     "dsd_batch_device_summaries", "dsd_stream", "dsd_last_launch_count", "dsd_last_kernel_ms",
     "dsd_last_transfer_bytes",
@@ -82,6 +83,9 @@ def lib():
     vp, sz, cp = c.c_void_p, c.c_size_t, c.c_char_p
     L.dsd_abi_version.restype = c.c_int
     L.dsd_create.argtypes = [c.c_int, c.POINTER(vp), cp, sz]
+    L.dsd_create_devices.argtypes = [c.POINTER(c.c_int), c.c_int, c.POINTER(vp), cp, sz]
+    L.dsd_device_count.argtypes = [vp]
+    L.dsd_batch_shard_sizes.argtypes = [vp, c.POINTER(c.c_int64), c.c_int]
     L.dsd_destroy.argtypes = [vp]
     L.dsd_destroy.restype = None
     L.dsd_free.argtypes = [vp]

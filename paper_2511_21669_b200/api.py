@@ -98,15 +98,20 @@ class SweepOutput:
 
 
 class Simulator:
-    """One libdsdsim handle bound to one CUDA device (dsd_create)."""
+    """One libdsdsim handle: one CUDA device (dsd_create) or a list of them
+    (dsd_create_devices; every batch / sweep is spread over all of them and
+    its results come back in replica order, as on one device)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device=0):
         L = _lib.lib()
         self._L = L
         self._h = ctypes.c_void_p()
         err = ctypes.create_string_buffer(1024)
-        _check(L.dsd_create(device, ctypes.byref(self._h), err, 1024), err)
-        self.device = device
+        devices = [int(d) for d in device] if isinstance(device, (list, tuple)) else [int(device)]
+        arr = (ctypes.c_int * len(devices))(*devices)
+        _check(L.dsd_create_devices(arr, len(devices), ctypes.byref(self._h), err, 1024), err)
+        self.devices = devices
+        self.device = devices[0]
 
     # ---- lifecycle ----
     def close(self):
@@ -189,6 +194,12 @@ class Simulator:
         if self._L.dsd_batch_device_summaries(self._h, ctypes.byref(p), ctypes.byref(b)) != 0:
             raise EngineError("no prepared batch")
         return p.value, b.value
+
+    def shard_sizes(self):
+        """Replicas of the prepared batch on each of the handle's devices."""
+        buf = (ctypes.c_int64 * 64)()
+        n = self._L.dsd_batch_shard_sizes(self._h, buf, 64)
+        return [int(buf[k]) for k in range(n)]
 
     def stream(self) -> int:
         return self._L.dsd_stream(self._h) or 0

@@ -1377,6 +1377,9 @@ struct Engine {
             if (tokens >= output) break;
             ++seq;  // IterationStart at now: scheduled, and the earliest event
         }
+#ifdef DSD_REP_STATS
+        if (W.rep_stats) W.rep_stats[3 * static_cast<int64_t>(rep) + 1] += static_cast<uint32_t>(nc - r.nc);
+#endif
         // where the last iteration stopped: the first event that is not the
         // replica's earliest is left pending (defer), the handlers before it ran
         int stage = 5;   // 5: the request completed

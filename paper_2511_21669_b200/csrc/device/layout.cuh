@@ -203,6 +203,9 @@ struct Workspace {
     // ---- optional step profile (DSD_STEP_STATS=1): [2k] cycles, [2k+1] count
     // per step kind, [32] warp iterations, [33] warp cycles, [34] max iterations
     unsigned long long* step_stats;
+    // ... and per replica [n][3]: vote rounds it ran in, session-loop
+    // iterations (builds with -DDSD_REP_STATS), cycles from init to finish
+    unsigned long long* rep_stats;
     // specialised kernel: run the active session's speculation loop directly
     // (Engine::session_run); env DSD_SESSION_FAST=0 disables it
     int32_t session_fast;

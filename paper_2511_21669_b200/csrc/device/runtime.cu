@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_
     // accumulation, flushed once per block
     __shared__ unsigned long long blk_stats[kStats ? 2 * kActKinds : 1];
     long long t_start = 0;
-    unsigned long long iters = 0;
+    unsigned long long iters = 0, my_rounds = 0;
     if constexpr (kStats) {
         for (int k = threadIdx.x; k < 2 * kActKinds; k += blockDim.x) blk_stats[k] = 0;
         __syncthreads();
@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_
             if ((threadIdx.x & (kLanes - 1)) == 0) atomicAdd(&W.step_stats[40 + vote_kind(best)], 1ull);
         }
         if (kind == vote_kind(best)) {
+            if constexpr (kStats) ++my_rounds;
             // the selected lanes run their continuation chain up to the next
             // barrier kind (kBarrierKinds)
             do {
@@ -221,6 +222,12 @@ __global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_
         for (int k = threadIdx.x; k < 2 * kActKinds; k += blockDim.x) atomicAdd(&W.step_stats[k], blk_stats[k]);
     }
     if (live) e.finish();
+    if constexpr (kStats) {
+        if (live && W.rep_stats) {
+            W.rep_stats[3 * rep] = my_rounds;
+            W.rep_stats[3 * rep + 2] = static_cast<unsigned long long>(clock64() - t_start);
+        }
+    }
 }
 
 // Session latency tables of the specialised kernel (Workspace::spec_lat):
@@ -314,7 +321,7 @@ struct RuntimeImpl {
     bool spec_ok = false;
     bool specialize = true;
     // shared-memory carveout of the kSmem kernels (% of the SM's maximum):
-    // -1 = sized per launch (Runtime::launch), env DSD_CARVEOUT fixes it
+    // -1 = sized per launch (DeviceRuntime::launch), env DSD_CARVEOUT fixes it
     int carveout = -1;
     // lane placement of the simulation kernel: [count][thread -> replica or
     // -1] (empty: replica = thread index)
@@ -349,7 +356,7 @@ struct RuntimeImpl {
     std::vector<int32_t> h_seqg, h_seqc;
 };
 
-Runtime::Runtime(int device) : impl_(new RuntimeImpl) {
+DeviceRuntime::DeviceRuntime(int device) : impl_(new RuntimeImpl) {
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess || count == 0)
@@ -382,7 +389,7 @@ Runtime::Runtime(int device) : impl_(new RuntimeImpl) {
     for (auto& ev : impl_->ev) DSD_CUDA(cudaEventCreate(&ev));
 }
 
-Runtime::~Runtime() {
+DeviceRuntime::~DeviceRuntime() {
     if (!impl_) return;
     cudaSetDevice(impl_->device);
     if (impl_->stream) cudaStreamSynchronize(impl_->stream);
@@ -392,36 +399,42 @@ Runtime::~Runtime() {
     if (impl_->stream) cudaStreamDestroy(impl_->stream);
 }
 
-void* Runtime::stream() { return impl_->stream; }
-int64_t Runtime::last_launch_count() const { return impl_->launches; }
-size_t Runtime::replica_count() const { return impl_->n; }
-void Runtime::transfer_bytes(int64_t* h2d, int64_t* d2h) const {
+void* DeviceRuntime::stream() { return impl_->stream; }
+int DeviceRuntime::device() const { return impl_->device; }
+int64_t DeviceRuntime::last_launch_count() const { return impl_->launches; }
+size_t DeviceRuntime::replica_count() const { return impl_->n; }
+void DeviceRuntime::transfer_bytes(int64_t* h2d, int64_t* d2h) const {
     if (h2d) *h2d = impl_->h2d_bytes;
     if (d2h) *d2h = impl_->d2h_bytes;
 }
 
-// Cost-aware lane placement: a warp advances at the pace of its
-// slowest lane, and a warp with fewer live lanes needs fewer vote rounds, so
-// the heaviest replicas get warps of 8 or 16 live lanes and the rest full
-// warps, as long as all warps stay resident in one wave (`warp_cap`).
-// Replicas are sorted by an estimate of their event count - for a
-// synthetic workload with a static window, N x (4 + 5 x median output /
-// E[tokens per round]) with E[tokens per round] = (1 - a^(g+1)) / (1 - a)
-// (the speculative-decoding expectation) - so warps are also homogeneous.
-// Returns [count][thread -> replica or -1], or nothing when every replica
-// looks alike or the batch already needs more than one wave.  Placement only
-// chooses which thread runs which replica: results are unchanged.
+// Cost-aware lane placement.  A warp advances at the pace of
+// its slowest lane, and the more lanes it carries the more vote rounds each
+// of them waits through: measured on the heaviest C5 replica (gamma 1, alpha
+// 0.5) alone, a warp of 1 / 2 / 4 / 8 / 16 lanes takes 1 / 1.68 / 2.54 /
+// 3.54 / 4.57 x the time of a lone lane (kWarpSlow).  Replicas are sorted by
+// an estimate of their cost - N x (9 + median output / E[tokens per round])
+// for a synthetic workload with a static window, E = (1 - a^(g+1)) / (1 - a):
+// about nine steps of general event handling per request plus one session
+// iteration per round - and each gets the widest warp that keeps
+// cost x kWarpSlow[width] within a makespan T, the smallest T whose warps
+// all fit one wave (`warp_cap`, binary search).  So a batch that leaves room
+// (a strong-scaling shard, a small sweep) runs its heavy replicas one per
+// warp, and a full one packs the light replicas 32 to a warp.  Sorting also
+// makes warps homogeneous.  Returns [count][thread -> replica or -1], or
+// nothing when the batch has no estimate or needs more than one wave.
+// Placement only chooses which thread runs which replica: results are
+// unchanged.
 static std::vector<int32_t> placement_list(const Packed& P, size_t n, int64_t warp_cap) {
-    if (n < 2 * kLanes) return {};
-    const int64_t dense = (static_cast<int64_t>(n) + kLanes - 1) / kLanes;
-    if (dense >= warp_cap) return {};
+    if (n < 2) return {};
+    if (static_cast<int64_t>(n) > warp_cap * kLanes) return {};
     std::vector<double> est(P.scen.size(), 0.0);
     for (size_t k = 0; k < P.scen.size(); ++k) {
         const DevScenario& d = P.scen[k];
         if (d.workload != 0 || d.n_drafts < 1 || d.fused_everything || d.window_kind != 0) return {};
         const double a = d.alpha, g = d.gamma;
         const double tau = a < 1.0 ? (1.0 - std::pow(a, g + 1.0)) / (1.0 - a) : g + 1.0;
-        est[k] = static_cast<double>(d.n_requests) * (4.0 + 5.0 * std::exp(d.o_mu) / tau);
+        est[k] = static_cast<double>(d.n_requests) * (9.0 + std::exp(d.o_mu) / tau);
     }
     // replicas by decreasing estimate: sort the scenarios, then a counting
     // sort of the replicas by their scenario's rank (replica order within one)
@@ -434,43 +447,52 @@ static std::vector<int32_t> placement_list(const Packed& P, size_t n, int64_t wa
     for (size_t i = 0; i < ns; ++i) start[i + 1] += start[i];
     std::vector<int32_t> order(n);
     for (size_t r = 0; r < n; ++r) order[static_cast<size_t>(start[static_cast<size_t>(srank[P.rep_scen[r]])]++)] = static_cast<int32_t>(r);
-    const double top = est[P.rep_scen[static_cast<size_t>(order[0])]];
-    if (!(top > 1.05 * est[P.rep_scen[static_cast<size_t>(order[n - 1])]])) return {};
-    // tiers: >= 90% of the heaviest -> 8 lanes, >= 75% -> 16 lanes, rest 32
-    // (DSD_PLACE_T8 / DSD_PLACE_T16); shrink the thin tiers until the warps
-    // fit one wave
-    static const double th8 = std::getenv("DSD_PLACE_T8") ? std::atof(std::getenv("DSD_PLACE_T8")) : 0.90;
-    static const double th16 = std::getenv("DSD_PLACE_T16") ? std::atof(std::getenv("DSD_PLACE_T16")) : 0.75;
-    int64_t t8 = 0, t16 = 0;
-    for (size_t i = 0; i < n; ++i) {
-        const double e = est[P.rep_scen[static_cast<size_t>(order[i])]];
-        if (e >= th8 * top) ++t8; else if (e >= th16 * top) ++t16;
-    }
-    auto warps = [&](int64_t a8, int64_t a16) {
-        return (a8 + 7) / 8 + (a16 + 15) / 16 + (static_cast<int64_t>(n) - a8 - a16 + kLanes - 1) / kLanes;
+    std::vector<double> cost(n);
+    for (size_t i = 0; i < n; ++i) cost[i] = est[P.rep_scen[static_cast<size_t>(order[i])]];
+    static const int kWidth[6] = {1, 2, 4, 8, 16, 32};
+    static const double kWarpSlow[6] = {1.0, 1.68, 2.54, 3.54, 4.57, 5.6};
+    // width of replica i under makespan T (-1: does not fit even alone)
+    auto width = [&](double c, double T) {
+        int w = -1;
+        for (int k = 0; k < 6; ++k)
+            if (c * kWarpSlow[k] <= T) w = k;
+        return w;
     };
-    while (warps(t8, t16) > warp_cap && (t8 > 0 || t16 > 0)) {
-        if (t8 > 0) {
-            const int64_t m = std::min<int64_t>(t8, 8);
-            t8 -= m;
-            t16 += m;
-        } else {
-            t16 -= std::min<int64_t>(t16, 16);
+    // warps needed: consecutive replicas (costs descending, widths
+    // ascending) of one width share warps
+    auto warps = [&](double T) {
+        int64_t total = 0, run = 0;
+        int cur = -2;
+        for (size_t i = 0; i < n; ++i) {
+            const int w = width(cost[i], T);
+            if (w < 0) return INT64_MAX;
+            if (w != cur) {
+                if (cur >= 0) total += (run + kWidth[cur] - 1) / kWidth[cur];
+                cur = w;
+                run = 0;
+            }
+            ++run;
         }
+        return total + (run + kWidth[cur] - 1) / kWidth[cur];
+    };
+    double lo = cost[0], hi = cost[0] * kWarpSlow[5];
+    if (warps(hi) > warp_cap) return {};
+    for (int it = 0; it < 40; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (warps(mid) <= warp_cap) hi = mid; else lo = mid;
     }
-    if (t8 == 0 && t16 == 0) return {};
+    const double T = hi;
+    if (width(cost[n - 1], T) == 5 && width(cost[0], T) == 5) return {};  // every warp full: the dense layout
     std::vector<int32_t> pl(1, 0);
-    size_t i = 0;
-    auto emit = [&](int64_t count, int lanes) {
-        for (int64_t done = 0; done < count;) {
-            for (int l = 0; l < kLanes; ++l)
-                pl.push_back(l < lanes && done < count ? order[i + static_cast<size_t>(done++)] : -1);
+    for (size_t i = 0; i < n;) {
+        const int w = width(cost[i], T);
+        size_t j = i;
+        while (j < n && width(cost[j], T) == w) ++j;
+        for (size_t k = i; k < j;) {
+            for (int l = 0; l < kLanes; ++l) pl.push_back(l < kWidth[w] && k < j ? order[k++] : -1);
         }
-        i += static_cast<size_t>(count);
-    };
-    emit(t8, 8);
-    emit(t16, 16);
-    emit(static_cast<int64_t>(n) - t8 - t16, kLanes);
+        i = j;
+    }
     pl[0] = static_cast<int32_t>(pl.size() - 1);
     return pl;
 }
@@ -516,7 +538,7 @@ static int64_t spec_lat_jobs(Packed& P, std::vector<SpecLatJob>& jobs) {
     return off;
 }
 
-void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n,
+void DeviceRuntime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n,
                       bool collect, bool feature_probe) {
     RuntimeImpl& R = *impl_;
     DSD_CUDA(cudaSetDevice(R.device));
@@ -633,7 +655,16 @@ static void place_lanes(RuntimeImpl& R) {
     const size_t n = R.n;
     const bool spec_launch = R.spec_ok && R.specialize && !R.collect && !R.W.probe;
     const int64_t max_blocks = spec_launch ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_BLOCKS;
-    std::vector<int32_t> pl = placement_list(R.packed, n, R.sms * max_blocks * (kBlock / kLanes));
+    // blocks one wave puts on an SM: the launch bounds, and for the
+    // shared-memory variant its per-block shared memory
+    int64_t per_sm = max_blocks;
+    if (R.W.c.ns <= kSmemServers && R.smem_heap > 0) {
+        const int64_t bytes = (kBlock / kLanes) * smem_warp_bytes(spec_launch ? 2 : R.W.c.ns, R.smem_heap,
+                                                                  R.W.c.awc != 0);
+        per_sm = std::max<int64_t>(1, std::min<int64_t>(max_blocks, R.smem_per_sm / (bytes + 1024)));
+    }
+    const int64_t warp_cap = R.sms * per_sm * (kBlock / kLanes);
+    std::vector<int32_t> pl = placement_list(R.packed, n, warp_cap);
     if (!pl.empty() && R.placement && R.lanes_per_warp == kLanes) {
         R.place.ensure(4 * pl.size());
         DSD_CUDA(cudaMemcpyAsync(R.place.p, pl.data(), 4 * pl.size(), cudaMemcpyHostToDevice, R.stream));
@@ -649,17 +680,8 @@ static void place_lanes(RuntimeImpl& R) {
     // 12,288 replicas -24 / -20 / -9 / -2%, but 24,576 replicas +12%.
     int64_t lpw = R.lanes_per_warp;
     if (R.place_n == 0 && R.placement && lpw == kLanes && n > 0 && R.spread &&
-        static_cast<double>(n) <= R.spread_max * R.sms * kLanes) {
-        const bool smem = R.W.c.ns <= kSmemServers && R.smem_heap > 0;
-        int64_t per_sm = max_blocks;
-        if (smem) {
-            const int64_t bytes = (kBlock / kLanes) * smem_warp_bytes(spec_launch ? 2 : R.W.c.ns, R.smem_heap,
-                                                                      R.W.c.awc != 0);
-            per_sm = std::max<int64_t>(1, std::min<int64_t>(max_blocks, R.smem_per_sm / (bytes + 1024)));
-        }
-        const int64_t cap = R.sms * per_sm * (kBlock / kLanes);
-        lpw = std::max<int64_t>(1, (static_cast<int64_t>(n) + cap - 1) / cap);
-    }
+        static_cast<double>(n) <= R.spread_max * R.sms * kLanes)
+        lpw = std::max<int64_t>(1, (static_cast<int64_t>(n) + warp_cap - 1) / warp_cap);
     if (lpw < kLanes && n > 0) {
         const int64_t nw = (static_cast<int64_t>(n) + lpw - 1) / lpw;
         std::vector<int32_t> ul(static_cast<size_t>(nw * kLanes + 1), -1);
@@ -673,7 +695,7 @@ static void place_lanes(RuntimeImpl& R) {
     }
 }
 
-void Runtime::launch() {
+void DeviceRuntime::launch() {
     RuntimeImpl& R = *impl_;
     if (!R.prepared) throw Error(DSD_ERR_RUNTIME, "launch without a prepared batch");
     DSD_CUDA(cudaSetDevice(R.device));
@@ -725,9 +747,10 @@ void Runtime::launch() {
         R.W.seq_commit = static_cast<int32_t*>(R.seqc.p);
     }
     if (R.step_stats) {
-        R.stats.ensure(64 * sizeof(unsigned long long));
-        DSD_CUDA(cudaMemsetAsync(R.stats.p, 0, 64 * sizeof(unsigned long long), R.stream));
+        R.stats.ensure((64 + 3 * R.n) * sizeof(unsigned long long));
+        DSD_CUDA(cudaMemsetAsync(R.stats.p, 0, (64 + 3 * R.n) * sizeof(unsigned long long), R.stream));
         R.W.step_stats = static_cast<unsigned long long*>(R.stats.p);
+        R.W.rep_stats = R.W.step_stats + 64;
     }
     DSD_CUDA(cudaEventRecord(R.ev[1], R.stream));
     const bool smem = R.W.c.ns <= kSmemServers && R.smem_heap > 0;
@@ -796,7 +819,7 @@ void Runtime::launch() {
     R.ran = true;
 }
 
-void Runtime::sync() {
+void DeviceRuntime::sync() {
     RuntimeImpl& R = *impl_;
     DSD_CUDA(cudaSetDevice(R.device));
     DSD_CUDA(cudaStreamSynchronize(R.stream));
@@ -809,6 +832,14 @@ void Runtime::sync() {
         unsigned long long s[64];
         static_assert(40 + kActKinds <= 64, "step stats layout");
         DSD_CUDA(cudaMemcpy(s, R.stats.p, sizeof(s), cudaMemcpyDeviceToHost));
+        if (const char* f = std::getenv("DSD_REP_STATS_FILE")) {  // per-replica [n][3], raw u64
+            std::vector<unsigned long long> rs(3 * R.n);
+            DSD_CUDA(cudaMemcpy(rs.data(), R.W.rep_stats, 8 * rs.size(), cudaMemcpyDeviceToHost));
+            if (FILE* fp = std::fopen(f, "wb")) {
+                std::fwrite(rs.data(), 8, rs.size(), fp);
+                std::fclose(fp);
+            }
+        }
         static const char* names[] = {"pop", "arrival", "net_prompt", "net_proposal", "net_result", "begin",
                                       "compute_done", "item", "finish", "activate", "dispatch", "send_prompt"};
         unsigned long long steps = 0;
@@ -823,7 +854,7 @@ void Runtime::sync() {
     }
 }
 
-void Runtime::last_kernel_ms(double* sim_ms, double* gen_ms, double* total_ms) {
+void DeviceRuntime::last_kernel_ms(double* sim_ms, double* gen_ms, double* total_ms) {
     RuntimeImpl& R = *impl_;
     float a = 0, b = 0;
     if (R.ran && R.n > 0) {
@@ -836,7 +867,7 @@ void Runtime::last_kernel_ms(double* sim_ms, double* gen_ms, double* total_ms) {
     if (gen_ms) *gen_ms = b - a;
 }
 
-void Runtime::summaries(dsd_replica_summary* out, size_t n) {
+void DeviceRuntime::summaries(dsd_replica_summary* out, size_t n) {
     RuntimeImpl& R = *impl_;
     if (!R.ran) throw Error(DSD_ERR_RUNTIME, "no completed batch");
     if (n > R.n) throw Error(DSD_ERR_RUNTIME, "summary buffer larger than the batch");
@@ -846,7 +877,7 @@ void Runtime::summaries(dsd_replica_summary* out, size_t n) {
     DSD_CUDA(cudaStreamSynchronize(R.stream));
 }
 
-const dsd_replica_summary* Runtime::host_summaries() {
+const dsd_replica_summary* DeviceRuntime::host_summaries() {
     RuntimeImpl& R = *impl_;
     if (!R.ran) throw Error(DSD_ERR_RUNTIME, "no completed batch");
     DSD_CUDA(cudaSetDevice(R.device));
@@ -867,7 +898,7 @@ const dsd_replica_summary* Runtime::host_summaries() {
 static_assert(kProbeFields == DSD_PROBE_FIELDS, "probe layout must match include/dsdsim.h");
 static_assert(sizeof(DevSummary) == sizeof(dsd_replica_summary), "summary layout must match include/dsdsim.h");
 
-void Runtime::probe(double* out, size_t n) {
+void DeviceRuntime::probe(double* out, size_t n) {
     RuntimeImpl& R = *impl_;
     if (!R.ran || !R.W.probe) throw Error(DSD_ERR_RUNTIME, "the batch did not run with the feature probe");
     if (n > R.n) n = R.n;
@@ -876,12 +907,12 @@ void Runtime::probe(double* out, size_t n) {
     if (n) DSD_CUDA(cudaMemcpy(out, R.W.probe, sizeof(double) * kProbeFields * n, cudaMemcpyDeviceToHost));
 }
 
-void Runtime::device_summaries(void** ptr, size_t* bytes) {
+void DeviceRuntime::device_summaries(void** ptr, size_t* bytes) {
     *ptr = impl_->summary.p;
     *bytes = sizeof(DevSummary) * impl_->n;
 }
 
-void Runtime::fetch_records(size_t replica, dsd_request_record* records, size_t cap,
+void DeviceRuntime::fetch_records(size_t replica, dsd_request_record* records, size_t cap,
                             int64_t* n_records, int32_t* gamma_seq, int32_t* committed_seq,
                             size_t seq_cap, int64_t* n_seq, int64_t* busy_us, size_t busy_cap) {
     RuntimeImpl& R = *impl_;

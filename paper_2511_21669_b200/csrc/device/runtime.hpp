@@ -21,12 +21,14 @@ struct Error : std::runtime_error {
 
 struct RuntimeImpl;
 
-class Runtime {
+// One GPU: packs a batch into its scenario blob + workspace and runs the
+// staging and simulation kernels on its own stream (runtime.cu).
+class DeviceRuntime {
 public:
-    explicit Runtime(int device);
-    ~Runtime();
-    Runtime(const Runtime&) = delete;
-    Runtime& operator=(const Runtime&) = delete;
+    explicit DeviceRuntime(int device);
+    ~DeviceRuntime();
+    DeviceRuntime(const DeviceRuntime&) = delete;
+    DeviceRuntime& operator=(const DeviceRuntime&) = delete;
 
     // Packs + uploads scenarios and replicas and sizes the workspace.
     // feature_probe: accumulate the per-replica probe sums (probe()).
@@ -46,6 +48,7 @@ public:
     // After a probed run: [n][kProbeFields] sums per replica (see Workspace::probe).
     void probe(double* out, size_t n);
     void* stream();
+    int device() const;
     int64_t last_launch_count() const;
     void last_kernel_ms(double* sim_ms, double* gen_ms, double* total_ms);
     size_t replica_count() const;
@@ -54,5 +57,63 @@ public:
 private:
     std::unique_ptr<RuntimeImpl> impl_;
 };
+
+// The engine behind a dsd_handle: one or more GPUs driven from one host
+// thread (multi.cpp).  A batch's replicas are dealt across the devices in
+// cost order (shard_of_replicas) and every call below keeps the
+// caller's replica numbering: summaries, records and probe sums come back in
+// the order the replicas were given.  With one device it is a thin
+// forwarder to its DeviceRuntime.
+class Runtime {
+public:
+    explicit Runtime(int device);
+    explicit Runtime(const std::vector<int>& devices);
+    ~Runtime();
+    Runtime(const Runtime&) = delete;
+    Runtime& operator=(const Runtime&) = delete;
+
+    void prepare(const dsd_scenario* scenarios, size_t n_scenarios, const dsd_replica* replicas,
+                 size_t n, bool collect_records, bool feature_probe = false);
+    void launch();
+    void sync();
+    void summaries(dsd_replica_summary* out, size_t n);
+    const dsd_replica_summary* host_summaries();
+    void fetch_records(size_t replica, dsd_request_record* records, size_t cap, int64_t* n_records,
+                       int32_t* gamma_seq, int32_t* committed_seq, size_t seq_cap, int64_t* n_seq,
+                       int64_t* busy_us, size_t busy_cap);
+    // single-device handles only (the benchmark's NCCL gather reads it)
+    void device_summaries(void** ptr, size_t* bytes);
+    void probe(double* out, size_t n);
+    void* stream();  // device 0's stream
+    int64_t last_launch_count() const;        // summed over the devices
+    void last_kernel_ms(double* sim_ms, double* gen_ms, double* total_ms);  // max over the devices
+    size_t replica_count() const;
+    void transfer_bytes(int64_t* h2d, int64_t* d2h) const;  // summed
+    size_t device_count() const { return devs_.size(); }
+    int device(size_t k) const { return devs_[k]->device(); }
+    // replicas of the prepared batch per device
+    std::vector<size_t> shard_sizes() const;
+
+private:
+    std::vector<std::unique_ptr<DeviceRuntime>> devs_;
+    // prepared batch: replica -> (device, index on it); per device its replicas' global indices
+    std::vector<int32_t> dev_of_;
+    std::vector<uint32_t> local_of_;
+    std::vector<std::vector<uint32_t>> global_of_;
+    std::vector<dsd_replica_summary> gathered_;
+    size_t n_ = 0;
+};
+
+// Estimated cost (simulated events) of one replica of a scenario: N x (4 +
+// 5 x median output / E[tokens per round]) for a synthetic workload with a
+// static window (E = (1 - a^(g+1)) / (1 - a)), N x (4 + 5 x mean output)
+// otherwise.  Only orders replicas; results never depend on it.
+double replica_cost_estimate(const dsd_scenario& s);
+// Shard of each replica when n replicas are spread over n_shards devices:
+// replicas sorted by decreasing cost (ties: lower index first) are dealt in
+// snake order 0..N-1, N-1..0, ..., so every shard gets the same count (+-1)
+// and a near-equal share of the heavy replicas.
+std::vector<int32_t> shard_of_replicas(const dsd_scenario* scenarios, const dsd_replica* replicas, size_t n,
+                                       int n_shards);
 
 }  // namespace dsd

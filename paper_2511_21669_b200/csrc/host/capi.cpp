@@ -71,12 +71,26 @@ int dsd_abi_version(void) { return DSD_ABI_VERSION; }
 void dsd_free(void* p) { std::free(p); }
 
 int dsd_create(int device_ordinal, dsd_handle** out, char* err, size_t errlen) {
+    return dsd_create_devices(&device_ordinal, 1, out, err, errlen);
+}
+
+int dsd_create_devices(const int* device_ordinals, int n_devices, dsd_handle** out, char* err, size_t errlen) {
     return guard(err, errlen, [&] {
         if (!out) throw dsd::Error(DSD_ERR_RUNTIME, "null output handle");
+        if (n_devices < 1 || !device_ordinals) throw dsd::Error(DSD_ERR_RUNTIME, "empty device list");
         auto h = std::make_unique<dsd_handle>();
-        h->rt = std::make_unique<dsd::Runtime>(device_ordinal);
+        h->rt = std::make_unique<dsd::Runtime>(std::vector<int>(device_ordinals, device_ordinals + n_devices));
         *out = h.release();
     });
+}
+
+int dsd_device_count(dsd_handle* h) { return (h && h->rt) ? static_cast<int>(h->rt->device_count()) : 0; }
+
+int dsd_batch_shard_sizes(dsd_handle* h, int64_t* sizes, int cap) {
+    if (!h || !h->rt) return 0;
+    const std::vector<size_t> s = h->rt->shard_sizes();
+    for (size_t k = 0; k < s.size() && static_cast<int>(k) < cap; ++k) sizes[k] = static_cast<int64_t>(s[k]);
+    return static_cast<int>(s.size());
 }
 
 void dsd_destroy(dsd_handle* h) { delete h; }
@@ -132,7 +146,7 @@ int dsd_batch_summaries(dsd_handle* h, dsd_replica_summary* summaries, size_t n,
 }
 
 int dsd_batch_device_summaries(dsd_handle* h, void** dev_ptr, size_t* bytes) {
-    if (!h || !h->rt || !dev_ptr || !bytes) return DSD_ERR_RUNTIME;
+    if (!h || !h->rt || !dev_ptr || !bytes || h->rt->device_count() != 1) return DSD_ERR_RUNTIME;
     h->rt->device_summaries(dev_ptr, bytes);
     return DSD_OK;
 }

@@ -1,0 +1,250 @@
+// multi.cpp — Runtime: one dsd_handle driving one or more GPUs from one host
+// thread (include/dsdsim.h dsd_create_devices).  The reference's run_sweep
+// spreads a sweep's (point, repetition) jobs over a thread pool
+// (proj/src/runner/sweep.cpp:109-160); here the replicas of a batch are
+// dealt across the devices in cost order and each device runs its share as
+// one batch, the shares running concurrently (one stream per device).  The
+// per-replica summaries come back into one host array in the caller's
+// replica order - the gather of SURVEY §8(e) done as per-device D2H copies
+// into page-locked memory, since one process owns every device here.
+#include <algorithm>
+#include <cmath>
+#include <exception>
+#include <mutex>
+#include <numeric>
+#include <thread>
+
+#include "../device/runtime.hpp"
+
+namespace dsd {
+
+double replica_cost_estimate(const dsd_scenario& s) {
+    double n = 0.0, out = 0.0;
+    if (s.workload == DSD_WORKLOAD_SYNTHETIC) {
+        n = static_cast<double>(s.n_requests);
+        out = s.output_median;
+    } else if (s.trace) {
+        n = static_cast<double>(s.trace->n);
+        double sum = 0.0;
+        for (int64_t i = 0; i < s.trace->n; ++i) sum += static_cast<double>(s.trace->output_length[i]);
+        out = s.trace->n > 0 ? sum / static_cast<double>(s.trace->n) : 0.0;
+    }
+    double tau = 1.0;
+    if (s.workload == DSD_WORKLOAD_SYNTHETIC && s.window_kind == DSD_WINDOW_STATIC && s.n_drafts > 0) {
+        const double a = s.acceptance_rate, g = s.gamma;
+        tau = a < 1.0 ? (1.0 - std::pow(a, g + 1.0)) / (1.0 - a) : g + 1.0;
+    }
+    return n * (4.0 + 5.0 * out / std::max(tau, 1e-9));
+}
+
+std::vector<int32_t> shard_of_replicas(const dsd_scenario* sc, const dsd_replica* reps, size_t n, int n_shards) {
+    std::vector<int32_t> shard(n, 0);
+    if (n_shards <= 1 || n == 0) return shard;
+    // cost per distinct scenario, then replicas by decreasing cost
+    std::vector<double> cost(n);
+    {
+        std::vector<double> sc_cost;
+        std::vector<char> have;
+        for (size_t k = 0; k < n; ++k) {
+            const uint32_t s = reps[k].scenario;
+            if (s >= sc_cost.size()) {
+                sc_cost.resize(s + 1, 0.0);
+                have.resize(s + 1, 0);
+            }
+            if (!have[s]) {
+                sc_cost[s] = replica_cost_estimate(sc[s]);
+                have[s] = 1;
+            }
+            cost[k] = sc_cost[s];
+        }
+    }
+    std::vector<uint32_t> order(n);
+    std::iota(order.begin(), order.end(), 0u);
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cost[a] > cost[b]; });
+    const size_t N = static_cast<size_t>(n_shards);
+    for (size_t i = 0; i < n; ++i) {
+        const size_t round = i / N, pos = i % N;
+        shard[order[i]] = static_cast<int32_t>(round % 2 == 0 ? pos : N - 1 - pos);
+    }
+    return shard;
+}
+
+Runtime::Runtime(int device) { devs_.push_back(std::make_unique<DeviceRuntime>(device)); }
+
+Runtime::Runtime(const std::vector<int>& devices) {
+    if (devices.empty()) throw Error(DSD_ERR_RUNTIME, "empty device list");
+    for (size_t i = 0; i < devices.size(); ++i)
+        for (size_t j = 0; j < i; ++j)
+            if (devices[i] == devices[j]) throw Error(DSD_ERR_RUNTIME, "device listed twice");
+    for (int d : devices) devs_.push_back(std::make_unique<DeviceRuntime>(d));
+}
+
+Runtime::~Runtime() = default;
+
+// fn(k) for every device, concurrently (one host thread per extra device);
+// the first exception is rethrown once all have finished
+template <class F>
+static void each_device(size_t n, F&& fn) {
+    if (n == 1) {
+        fn(size_t{0});
+        return;
+    }
+    std::exception_ptr first;
+    std::mutex m;
+    auto run = [&](size_t k) {
+        try {
+            fn(k);
+        } catch (...) {
+            std::lock_guard<std::mutex> g(m);
+            if (!first) first = std::current_exception();
+        }
+    };
+    std::vector<std::thread> th;
+    for (size_t k = 1; k < n; ++k) th.emplace_back(run, k);
+    run(0);
+    for (auto& t : th) t.join();
+    if (first) std::rethrow_exception(first);
+}
+
+void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n, bool collect,
+                      bool feature_probe) {
+    n_ = n;
+    gathered_.clear();
+    if (devs_.size() == 1) {
+        devs_[0]->prepare(sc, ns, reps, n, collect, feature_probe);
+        return;
+    }
+    const size_t D = devs_.size();
+    dev_of_ = shard_of_replicas(sc, reps, n, static_cast<int>(D));
+    local_of_.resize(n);
+    global_of_.assign(D, {});
+    for (size_t k = 0; k < n; ++k) {
+        std::vector<uint32_t>& g = global_of_[static_cast<size_t>(dev_of_[k])];
+        local_of_[k] = static_cast<uint32_t>(g.size());
+        g.push_back(static_cast<uint32_t>(k));
+    }
+    each_device(D, [&](size_t d) {
+        std::vector<dsd_replica> mine(global_of_[d].size());
+        for (size_t j = 0; j < mine.size(); ++j) mine[j] = reps[global_of_[d][j]];
+        devs_[d]->prepare(sc, ns, mine.data(), mine.size(), collect, feature_probe);
+    });
+}
+
+void Runtime::launch() {
+    gathered_.clear();
+    if (devs_.size() == 1) {
+        devs_[0]->launch();
+        return;
+    }
+    // launch() computes the lane placement on the host while k_stage runs:
+    // one host thread per device keeps the devices' launches overlapped
+    each_device(devs_.size(), [&](size_t d) { devs_[d]->launch(); });
+}
+
+void Runtime::sync() {
+    for (auto& d : devs_) d->sync();
+}
+
+const dsd_replica_summary* Runtime::host_summaries() {
+    if (devs_.size() == 1) return devs_[0]->host_summaries();
+    if (gathered_.size() != n_) {
+        gathered_.resize(n_);
+        each_device(devs_.size(), [&](size_t d) {
+            const dsd_replica_summary* s = devs_[d]->host_summaries();
+            const std::vector<uint32_t>& g = global_of_[d];
+            for (size_t j = 0; j < g.size(); ++j) gathered_[g[j]] = s[j];
+        });
+    }
+    return gathered_.data();
+}
+
+void Runtime::summaries(dsd_replica_summary* out, size_t n) {
+    if (devs_.size() == 1) {
+        devs_[0]->summaries(out, n);
+        return;
+    }
+    if (n > n_) throw Error(DSD_ERR_RUNTIME, "summary buffer larger than the batch");
+    const dsd_replica_summary* s = host_summaries();
+    std::copy(s, s + n, out);
+}
+
+void Runtime::fetch_records(size_t replica, dsd_request_record* records, size_t cap, int64_t* n_records,
+                            int32_t* gamma_seq, int32_t* committed_seq, size_t seq_cap, int64_t* n_seq,
+                            int64_t* busy_us, size_t busy_cap) {
+    if (devs_.size() == 1) {
+        devs_[0]->fetch_records(replica, records, cap, n_records, gamma_seq, committed_seq, seq_cap, n_seq, busy_us,
+                                busy_cap);
+        return;
+    }
+    if (replica >= n_) throw Error(DSD_ERR_RUNTIME, "replica index out of range");
+    devs_[static_cast<size_t>(dev_of_[replica])]->fetch_records(local_of_[replica], records, cap, n_records,
+                                                                 gamma_seq, committed_seq, seq_cap, n_seq, busy_us,
+                                                                 busy_cap);
+}
+
+void Runtime::device_summaries(void** ptr, size_t* bytes) {
+    if (devs_.size() != 1) throw Error(DSD_ERR_RUNTIME, "device summaries of a multi-device handle");
+    devs_[0]->device_summaries(ptr, bytes);
+}
+
+void Runtime::probe(double* out, size_t n) {
+    if (devs_.size() == 1) {
+        devs_[0]->probe(out, n);
+        return;
+    }
+    if (n > n_) n = n_;
+    std::vector<std::vector<double>> part(devs_.size());
+    each_device(devs_.size(), [&](size_t d) {
+        part[d].resize(global_of_[d].size() * DSD_PROBE_FIELDS);
+        devs_[d]->probe(part[d].data(), global_of_[d].size());
+    });
+    for (size_t k = 0; k < n; ++k) {
+        const double* src = part[static_cast<size_t>(dev_of_[k])].data() + static_cast<size_t>(local_of_[k]) * DSD_PROBE_FIELDS;
+        std::copy(src, src + DSD_PROBE_FIELDS, out + k * DSD_PROBE_FIELDS);
+    }
+}
+
+void* Runtime::stream() { return devs_[0]->stream(); }
+
+int64_t Runtime::last_launch_count() const {
+    int64_t s = 0;
+    for (const auto& d : devs_) s += d->last_launch_count();
+    return s;
+}
+
+void Runtime::last_kernel_ms(double* sim_ms, double* gen_ms, double* total_ms) {
+    double a = 0, b = 0, c = 0;
+    for (auto& d : devs_) {
+        double x = 0, y = 0, z = 0;
+        d->last_kernel_ms(&x, &y, &z);
+        a = std::max(a, x);
+        b = std::max(b, y);
+        c = std::max(c, z);
+    }
+    if (sim_ms) *sim_ms = a;
+    if (gen_ms) *gen_ms = b;
+    if (total_ms) *total_ms = c;
+}
+
+size_t Runtime::replica_count() const { return n_; }
+
+void Runtime::transfer_bytes(int64_t* h2d, int64_t* d2h) const {
+    int64_t a = 0, b = 0;
+    for (const auto& d : devs_) {
+        int64_t x = 0, y = 0;
+        d->transfer_bytes(&x, &y);
+        a += x;
+        b += y;
+    }
+    if (h2d) *h2d = a;
+    if (d2h) *d2h = b;
+}
+
+std::vector<size_t> Runtime::shard_sizes() const {
+    if (devs_.size() == 1) return {n_};
+    std::vector<size_t> s;
+    for (const auto& g : global_of_) s.push_back(g.size());
+    return s;
+}
+
+}  // namespace dsd

@@ -267,22 +267,18 @@ static void plan_points(SweepBatch& b, size_t lo, size_t hi, int shard, int n_sh
     // one work-stealing worker per thread (points differ in cost)
     parallel_chunks(n_points < 64 ? 1 : std::min<size_t>(n_points, host_threads()), 1, worker);
     tm.lap("points");
-    // resolved scenarios in point order, then the replicas of this shard:
-    // global replica g = scenario * repetitions + rep, kept when g % n_shards
-    // == shard, at position g / n_shards
+    // resolved scenarios in point order, then the replicas: global replica
+    // g = scenario * repetitions + rep (point-major)
     b.point_scenario.assign(n_points, -1);
     size_t n_ok = 0;
     for (size_t idx = 0; idx < n_points; ++idx)
         if (ok[idx]) b.point_scenario[idx] = static_cast<int64_t>(n_ok++);
     const size_t R = static_cast<size_t>(spec.repetitions);
-    const size_t N = n_shards > 1 ? static_cast<size_t>(n_shards) : 1;
-    const size_t sh = n_shards > 1 ? static_cast<size_t>(shard) : 0;
     const size_t n_rep = n_ok * R;
-    const size_t mine = n_rep > sh ? (n_rep - sh - 1) / N + 1 : 0;
     b.resolved.resize(n_ok);
     b.scenarios.resize(n_ok);
-    b.replicas.resize(mine);
-    b.replica_origin.resize(mine);
+    b.replicas.resize(n_rep);
+    b.replica_origin.resize(n_rep);
     parallel_chunks(n_points, 256, [&](size_t lo, size_t hi) {
         for (size_t idx = lo; idx < hi; ++idx) {
             const int64_t s = b.point_scenario[idx];
@@ -293,16 +289,29 @@ static void plan_points(SweepBatch& b, size_t lo, size_t hi, int shard, int n_sh
             b.scenarios[static_cast<size_t>(s)] = r.scen;
             for (size_t rep = 0; rep < R; ++rep) {
                 const size_t g = static_cast<size_t>(s) * R + rep;
-                if (g % N != sh) continue;
-                dsd_replica& x = b.replicas[g / N];
+                dsd_replica& x = b.replicas[g];
                 x = dsd_replica{};
                 x.scenario = static_cast<uint32_t>(s);
                 x.seed = seeds[idx][rep];
                 x.gen_seed = r.gen_seed_fixed ? r.gen_seed : x.seed;
-                b.replica_origin[g / N] = {static_cast<int64_t>(idx), static_cast<int>(rep)};
+                b.replica_origin[g] = {static_cast<int64_t>(idx), static_cast<int>(rep)};
             }
         }
     });
+    if (n_shards > 1) {
+        // one shard: the replicas shard_of_replicas deals to it (the split a
+        // multi-device handle makes), kept in point-major order
+        const std::vector<int32_t> sh = shard_of_replicas(b.scenarios.data(), b.replicas.data(), n_rep, n_shards);
+        size_t w = 0;
+        for (size_t g = 0; g < n_rep; ++g) {
+            if (sh[g] != shard) continue;
+            b.replicas[w] = b.replicas[g];
+            b.replica_origin[w] = b.replica_origin[g];
+            ++w;
+        }
+        b.replicas.resize(w);
+        b.replica_origin.resize(w);
+    }
     tm.lap("replicas");
 }
 

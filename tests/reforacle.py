@@ -44,6 +44,8 @@ def lib():
                                     c.POINTER(c.c_void_p), c.c_char_p, c.c_size_t]
         L.ref_sweep_point_seed.restype = c.c_uint64
         L.ref_sweep_point_seed.argtypes = [c.c_uint64, c.c_char_p, c.c_int]
+        L.ref_sweep_replicas.argtypes = [c.c_char_p, c.c_char_p, c.c_int, c.POINTER(c.c_double), c.c_char_p,
+                                         c.c_size_t]
         L.ref_sweep_bench.argtypes = [c.c_char_p, c.c_char_p, c.c_int, c.POINTER(c.c_int64), c.c_int64,
                                       c.POINTER(c.c_double), c.c_char_p, c.c_size_t]
         L.ref_random_model.argtypes = [c.c_uint64, c.c_int, c.c_int, c.POINTER(c.c_double),
@@ -118,6 +120,20 @@ def run_sweep(sweep_yaml, base_dir=".", parallel=8, out_dir=""):
     if rc != 0:
         raise RefError(rc, err.value.decode())
     return _take(js), _take(cs)
+
+
+def sweep_replicas(sweep_yaml, base_dir, threads, n_replicas):
+    """Per-replica results of the reference run_sweep worker, point-major:
+    float64 [n_replicas, 6] = events_processed, end_time, completed,
+    throughput_rps, mean_ttft_ms, mean_tpot_ms (failed points: -1)."""
+    import numpy as np
+    rows = np.zeros((n_replicas, 6), dtype=np.float64)
+    err = ctypes.create_string_buffer(4096)
+    rc = lib().ref_sweep_replicas(sweep_yaml.encode(), base_dir.encode(), threads,
+                                  rows.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), err, 4096)
+    if rc != 0:
+        raise RuntimeError(err.value.decode())
+    return rows
 
 
 def sweep_bench(sweep_yaml, base_dir, threads, points=None):

@@ -117,6 +117,28 @@ def test_full_c5_sweep_matches_reference():
     assert out.summary_csv == cs
 
 
+def test_full_c5_per_replica_matches_reference():
+    """Every one of the 65,536 C5 replicas, as the benchmark runs them (the
+    specialised kernel with the session fast path, no record collection):
+    events_processed, end_time and the RunAggregates (completed, throughput,
+    mean TTFT / TPOT) must equal the reference run_sweep worker's bit for bit."""
+    import numpy as np
+    from paper_2511_21669_b200 import Simulator
+    spec = open(os.path.join(CFG, "c5_sweep_65536.yaml")).read()
+    rows = ref.sweep_replicas(spec, CFG, os.cpu_count() or 8, 65536)
+    with Simulator(0) as s:
+        n, _ = s.prepare_sweep(spec, base_dir=CFG)
+        s.launch()
+        s.sync()
+        sm = s.summaries()
+    assert n == 65536 and (sm["status"] == 0).all()
+    np.testing.assert_array_equal(sm["events_processed"].astype(np.float64), rows[:, 0])
+    np.testing.assert_array_equal(sm["end_time_us"].astype(np.float64), rows[:, 1])
+    np.testing.assert_array_equal(sm["completed"].astype(np.float64), rows[:, 2])
+    for k, f in ((3, "throughput_rps"), (4, "mean_ttft_ms"), (5, "mean_tpot_ms")):
+        assert sm[f].tobytes() == rows[:, k].tobytes(), f
+
+
 def test_large_sweep_parallel_aggregation_matches_reference():
     """A sweep above the host's parallel thresholds (4,096 replicas for the
     per-point sums, 1,024 points for the summary text): sums split across host

@@ -105,3 +105,22 @@ def test_gloo_two_ranks_rebuild_reference_summary(tmp_path):
         assert w["throughput_rps"] == "%.6f" % thr or float(w["throughput_rps"]) == float("%.6f" % thr)
         assert float(w["mean_ttft_ms"]) == float("%.3f" % ttft)
         assert float(w["mean_tpot_ms"]) == float("%.3f" % tpot)
+
+
+def test_cost_ordered_shards_partition_the_sweep():
+    """dsd_plan_sweep's shards (the deal dsd_create_devices makes) partition
+    the sweep, each in point-major order, sizes within one of each other."""
+    spec = ("base: c1_single_pair.yaml\nseed: 5\nrepetitions: 3\naxes:\n"
+            "  policies.window.gamma: [1, 4, 16]\n  workload.acceptance_rate: [0.5, 0.9]\n  network.rtt_ms: [2, 30]\n")
+    _, _, _, _, n_all, pts_all, reps_all = plan_shard(spec, ref.CONFIGS, 0, 1)
+    for world in (2, 3, 4, 8):
+        seen = []
+        sizes = []
+        for shard in range(world):
+            _, _, _, _, n, pts, reps = plan_shard(spec, ref.CONFIGS, shard, world)
+            origin = list(zip(pts, reps))
+            assert origin == sorted(origin)
+            seen += origin
+            sizes.append(n)
+        assert sorted(seen) == sorted(zip(pts_all, reps_all))
+        assert max(sizes) - min(sizes) <= 1
