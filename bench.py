@@ -395,8 +395,11 @@ def main_ours(args, rank, world, local_rank):
 
     # ---- e2e through the public C ABI with host buffers: the drop-in call ----
     e2e_s, h2d, d2h, e2e_path = None, 0, 0, "dsd_run_sweep"
+    # the other ranks wait on a host (gloo) barrier: an NCCL barrier would
+    # spin a kernel on the GPUs rank 0 is now using
+    cpu_group = dist.new_group(backend="gloo") if dist else None
     if dist:
-        dist.barrier()
+        dist.barrier(group=cpu_group)
     if rank == 0:
         devices = list(range(world))
         esim = sim if world == 1 else Simulator(devices)
@@ -416,7 +419,7 @@ def main_ours(args, rank, world, local_rank):
         if esim is not sim:
             esim.close()
     if dist:
-        dist.barrier()
+        dist.barrier(group=cpu_group)
     if rank != 0:
         dist.destroy_process_group()
         return

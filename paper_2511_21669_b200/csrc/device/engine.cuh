@@ -472,7 +472,17 @@ enum : uint32_t {
      (1u << kActNetResult) | (1u << kActBeginAwc) | (1u << kActNone))
 #endif
 constexpr uint32_t kBarrierKinds = DSD_BARRIER_KINDS;
-DSD_HD bool is_barrier(uint32_t kind) { return (kBarrierKinds >> kind) & 1u; }
+// The specialised kernel's barrier: only the session loop's entry (Begin).
+// The loop absorbs the steady state, so what remains between two loop runs
+// is a short chain of per-request general events, which each lane now runs
+// in one go: every warp round is one loop run + one chain for all lanes.
+// Measured on the C5 sweep (B200): the general set 18.6 ms, {Begin} 14.2,
+// {Begin, Dispatch} 14.2, {Begin, Item} 14.6.
+#ifndef DSD_SPEC_BARRIER_KINDS
+#define DSD_SPEC_BARRIER_KINDS ((1u << kActBegin) | (1u << kActNone))
+#endif
+constexpr uint32_t kSpecBarrierKinds = DSD_SPEC_BARRIER_KINDS;
+DSD_HD bool is_barrier(uint32_t kind, bool spec) { return ((spec ? kSpecBarrierKinds : kBarrierKinds) >> kind) & 1u; }
 
 struct Engine {
     // Register budget: everything below stays live across the whole event
@@ -1762,7 +1772,7 @@ struct Engine {
         if (st0 == kStackEmpty) {
             pop_event();
             // a handler that is not a vote barrier runs in the same step
-            if (st0 == kStackEmpty || is_barrier(st0 & 15u)) return;
+            if (st0 == kStackEmpty || is_barrier(st0 & 15u, spec)) return;
         }
         const uint32_t a = pop_act();
         const uint32_t arg = a >> 4;

@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_
                     e.step();
                 }
                 kind = e.next_kind_unchecked();
-            } while (!((kBarrierKinds >> kind) & 1u));
+            } while (!(((kSpec ? kSpecBarrierKinds : kBarrierKinds) >> kind) & 1u));
             // (a failed replica stops at its next pop: next_kind_unchecked)
         }
         if constexpr (kStats) ++iters;
