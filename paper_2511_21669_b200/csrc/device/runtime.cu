@@ -260,6 +260,13 @@ __global__ void k_collect_overflow(Workspace W, int32_t* list, int32_t* count) {
     if (W.fail[rep] == kFailHeap || W.fail[rep] == kFailStack) list[atomicAdd(count, 1)] = static_cast<int32_t>(rep);
 }
 
+// Collects the replicas that failed with one failure code.
+__global__ void k_collect_fail(Workspace W, int32_t code, int32_t* list, int32_t* count) {
+    const int64_t rep = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (rep >= W.c.n) return;
+    if (W.fail[rep] == code) list[atomicAdd(count, 1)] = static_cast<int32_t>(rep);
+}
+
 __global__ void k_export(Workspace W, DevRecord* rec, int64_t* busy) {
     int64_t rep = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (rep >= W.c.n) return;
@@ -310,6 +317,7 @@ struct RuntimeImpl {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[4] = {};
     DevBuf blob, scen, reps, arena, summary, fail, ltot, seqbase, seqg, seqc, rec, busy, ovf, probe, slat, sjobs;
+    DevBuf heap2, ovf2;  // retry_heap_overflows: the larger event heap, its replica list
     // shared-memory heap slots per replica for small topologies (0 = always
     // run the HBM variant; env DSD_SMEM_HEAP overrides, for tests)
     // 7: with 8 server fields x 2 servers and one session slot a warp needs
@@ -348,6 +356,8 @@ struct RuntimeImpl {
     bool session_fast = true;        // Engine::session_run in the specialised kernel (DSD_SESSION_FAST=0: off)
     bool smem_launch = false;
     void* pinned = nullptr;  // host_summaries() buffer (page-locked)
+    bool pinned_valid = false;  // it holds the last launch's summaries
+    bool retried = false;       // sync() ran retry_heap_overflows for the last launch
     size_t pinned_bytes = 0;  // the last launch ran the shared-memory variant (+ HBM re-run)
     // records cache (filled lazily after a collect run)
     bool rec_cached = false;
@@ -545,6 +555,7 @@ void DeviceRuntime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica
     R.prepared = false;
     R.ran = false;
     R.rec_cached = false;
+    R.pinned_valid = false;
     // DSD_HOST_TIMING=1: phase durations to stderr
     static const bool timing = std::getenv("DSD_HOST_TIMING") != nullptr;
     auto t_prev = std::chrono::steady_clock::now();
@@ -558,6 +569,8 @@ void DeviceRuntime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica
     Packed& P = R.packed;
     pack_batch_into(P, sc, ns, reps, n, feature_probe);
     lap("pack");
+    // tests: a smaller HBM event heap (forces retry_heap_overflows)
+    if (const char* h = std::getenv("DSD_HEAP_CAP")) P.caps.hc = std::max<int64_t>(1, std::atoll(h));
     const Caps& c = P.caps;
     // every scenario fits the single-pair specialisation (Engine::spec)
     R.spec_ok = c.ns == 2;
@@ -701,6 +714,8 @@ void DeviceRuntime::launch() {
     DSD_CUDA(cudaSetDevice(R.device));
     R.launches = 0;
     R.rec_cached = false;
+    R.pinned_valid = false;
+    R.retried = false;
     if (R.n == 0) {
         R.ran = true;
         return;
@@ -819,10 +834,60 @@ void DeviceRuntime::launch() {
     R.ran = true;
 }
 
+// The HBM variant's event heap holds Caps::hc = 2 x requests + 8 x servers +
+// 64 pending events per replica.  That covers every pending event but the
+// stale BatchReady timers a full-batch dispatch leaves behind when it
+// disarms a batching window (engine.cpp:508-519): a window much longer than
+// the service time can pile them up past hc.  Replicas that overflowed
+// (kFailHeap after the HBM pass) run again with the heap doubled, in a
+// separate heap buffer and otherwise the same workspace, until none
+// overflows or the device has no room left for a larger heap.
+static void retry_heap_overflows(RuntimeImpl& R) {
+    int64_t hc = R.W.c.hc;
+    const unsigned grid = static_cast<unsigned>((R.n + kBlock - 1) / kBlock);
+    for (;;) {
+        R.ovf2.ensure(4 * (R.n + 1));
+        int32_t* count = static_cast<int32_t*>(R.ovf2.p);
+        int32_t* list = count + 1;
+        DSD_CUDA(cudaMemsetAsync(count, 0, 4, R.stream));
+        k_collect_fail<<<static_cast<unsigned>((R.n + 255) / 256), 256, 0, R.stream>>>(R.W, kFailHeap, list, count);
+        int32_t nfail = 0;
+        DSD_CUDA(cudaMemcpyAsync(&nfail, count, 4, cudaMemcpyDeviceToHost, R.stream));
+        DSD_CUDA(cudaStreamSynchronize(R.stream));
+        if (nfail == 0) return;
+        hc *= 2;
+        if (std::getenv("DSD_HOST_TIMING"))
+            std::fprintf(stderr, "[dsd sync] event heap overflow: %d replicas again with a heap of %lld\n", nfail,
+                         static_cast<long long>(hc));
+        const size_t slots = static_cast<size_t>(R.W.c.nwarps) * kLanes * static_cast<size_t>(hc);
+        const size_t bytes = slots * (sizeof(int64_t) + sizeof(uint64_t));
+        if (bytes > R.heap2.bytes) {
+            size_t free_b = 0, total_b = 0;
+            DSD_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            if (bytes + (256u << 20) > free_b + R.heap2.bytes) return;  // the replicas stay failed
+        }
+        R.heap2.ensure(bytes);
+        Workspace W2 = R.W;
+        W2.c.hc = hc;
+        W2.h_time = static_cast<int64_t*>(R.heap2.p);
+        W2.h_key = reinterpret_cast<uint64_t*>(W2.h_time + slots);
+        const size_t hbm_smem = R.W.c.awc ? (kBlock / kLanes) * sizeof(AwcWarpScratch) : 0;
+        k_stage<<<grid, kBlock, 0, R.stream>>>(W2, nullptr, list, count);
+        (R.W.c.awc ? k_simulate<false, false, false, true> : k_simulate<false, false>)<<<grid, kBlock, hbm_smem,
+                                                                                           R.stream>>>(W2, list, count, 0);
+        DSD_CUDA(cudaGetLastError());
+        R.launches += 3;
+    }
+}
+
 void DeviceRuntime::sync() {
     RuntimeImpl& R = *impl_;
     DSD_CUDA(cudaSetDevice(R.device));
     DSD_CUDA(cudaStreamSynchronize(R.stream));
+    if (R.ran && R.n > 0 && !R.retried) {
+        retry_heap_overflows(R);
+        R.retried = true;
+    }
     if (R.ran && R.n > 0 && R.smem_launch && std::getenv("DSD_HOST_TIMING")) {  // replicas the shared-memory kernel handed to the HBM variant
         int32_t rerun = 0;
         DSD_CUDA(cudaMemcpy(&rerun, R.ovf.p, sizeof(rerun), cudaMemcpyDeviceToHost));
@@ -871,7 +936,7 @@ void DeviceRuntime::summaries(dsd_replica_summary* out, size_t n) {
     RuntimeImpl& R = *impl_;
     if (!R.ran) throw Error(DSD_ERR_RUNTIME, "no completed batch");
     if (n > R.n) throw Error(DSD_ERR_RUNTIME, "summary buffer larger than the batch");
-    DSD_CUDA(cudaSetDevice(R.device));
+    sync();  // (and the heap-overflow retries)
     if (n) DSD_CUDA(cudaMemcpyAsync(out, R.summary.p, sizeof(DevSummary) * n, cudaMemcpyDeviceToHost, R.stream));
     R.d2h_bytes += static_cast<int64_t>(sizeof(DevSummary) * n);
     DSD_CUDA(cudaStreamSynchronize(R.stream));
@@ -889,9 +954,12 @@ const dsd_replica_summary* DeviceRuntime::host_summaries() {
         DSD_CUDA(cudaMallocHost(&R.pinned, bytes));
         R.pinned_bytes = bytes;
     }
+    if (R.pinned_valid) return static_cast<const dsd_replica_summary*>(R.pinned);
+    sync();
     if (R.n) DSD_CUDA(cudaMemcpyAsync(R.pinned, R.summary.p, sizeof(DevSummary) * R.n, cudaMemcpyDeviceToHost, R.stream));
     R.d2h_bytes += static_cast<int64_t>(sizeof(DevSummary) * R.n);
     DSD_CUDA(cudaStreamSynchronize(R.stream));
+    R.pinned_valid = true;
     return static_cast<const dsd_replica_summary*>(R.pinned);
 }
 
@@ -902,8 +970,7 @@ void DeviceRuntime::probe(double* out, size_t n) {
     RuntimeImpl& R = *impl_;
     if (!R.ran || !R.W.probe) throw Error(DSD_ERR_RUNTIME, "the batch did not run with the feature probe");
     if (n > R.n) n = R.n;
-    DSD_CUDA(cudaSetDevice(R.device));
-    DSD_CUDA(cudaStreamSynchronize(R.stream));
+    sync();
     if (n) DSD_CUDA(cudaMemcpy(out, R.W.probe, sizeof(double) * kProbeFields * n, cudaMemcpyDeviceToHost));
 }
 
@@ -918,7 +985,7 @@ void DeviceRuntime::fetch_records(size_t replica, dsd_request_record* records, s
     RuntimeImpl& R = *impl_;
     if (!R.ran || !R.collect) throw Error(DSD_ERR_RUNTIME, "records were not collected for this batch");
     if (replica >= R.n) throw Error(DSD_ERR_RUNTIME, "replica index out of range");
-    DSD_CUDA(cudaSetDevice(R.device));
+    sync();  // (and the heap-overflow retries)
     const Caps& c = R.W.c;
     if (!R.rec_cached) {
         R.rec.ensure(sizeof(DevRecord) * static_cast<size_t>(c.nr) * R.n);
@@ -941,9 +1008,10 @@ void DeviceRuntime::fetch_records(size_t replica, dsd_request_record* records, s
     }
     const DevScenario& S = R.packed.scen[0];
     (void)S;
-    dsd_replica_summary sm;
-    DSD_CUDA(cudaMemcpy(&sm, static_cast<DevSummary*>(R.summary.p) + replica, sizeof(sm), cudaMemcpyDeviceToHost));
-    const int64_t N = sm.n_requests;
+    // the batch's summaries come back once, in bulk (host_summaries), not one
+    // blocking copy per call
+    if (!R.pinned_valid) host_summaries();
+    const int64_t N = static_cast<const dsd_replica_summary*>(R.pinned)[replica].n_requests;
     if (n_records) *n_records = N;
     const DevRecord* src = R.h_rec.data() + replica * c.nr;
     if (records) {

@@ -12,6 +12,7 @@
 // -> DSD_ERR_CONFIG; IoError and the rest -> DSD_ERR_RUNTIME).
 #include "resolve.hpp"
 
+#include <sys/stat.h>
 #include <algorithm>
 #include <cmath>
 #include <fstream>
@@ -501,6 +502,20 @@ void Resolved::bind() {
 
 namespace {
 
+// Cache key of a file-backed input: its path plus size and modification
+// time, so a model / trace / profile rewritten at the same path between two
+// calls on one handle is read again (the reference re-reads every input on
+// each resolve_config, runner.cpp:96-134).  A file that cannot be stat'ed
+// keys by path alone (its loader reports the error).
+std::string file_key(const std::string& path) {
+    struct stat st;
+    if (::stat(path.c_str(), &st) != 0) return path;
+    return path + "|" + std::to_string(static_cast<long long>(st.st_size)) + "|" +
+           std::to_string(static_cast<long long>(st.st_mtim.tv_sec)) + "." +
+           std::to_string(static_cast<long long>(st.st_mtim.tv_nsec)) + "|" +
+           std::to_string(static_cast<unsigned long long>(st.st_ino));
+}
+
 template <typename T, typename F>
 std::shared_ptr<const T> cached(Caches* caches, std::map<std::string, std::shared_ptr<const T>> Caches::*slot,
                                 const std::string& key, F&& make) {
@@ -531,7 +546,7 @@ Resolved resolve_config(const Node& config, bool strict, std::optional<uint64_t>
             config_error("config requires 'latency_profile' (a path or an inline synth spec)");
         if (node->scalar()) {
             const std::string path = join_path(base_dir, node->to_string());
-            rc.profile = cached(caches, &Caches::profiles, "file:" + path, [&] { return load_profile_file(path); });
+            rc.profile = cached(caches, &Caches::profiles, "file:" + file_key(path), [&] { return load_profile_file(path); });
         } else if (node->map() && node->has("synth")) {
             const Node& s = *node->get("synth");
             if (strict) {
@@ -559,7 +574,7 @@ Resolved resolve_config(const Node& config, bool strict, std::optional<uint64_t>
     if (pol.window == DSD_WINDOW_AWC && !topo.drafts.empty()) {
         if (pol.model_path.empty()) config_error("window policy 'awc' requires policies.window.model");
         const std::string path = join_path(base_dir, pol.model_path);
-        rc.awc = cached(caches, &Caches::models, path, [&] { return load_model_file(path); });
+        rc.awc = cached(caches, &Caches::models, file_key(path), [&] { return load_model_file(path); });
     }
     dsd_scenario& s = rc.scen;
     s = dsd_scenario{};
@@ -580,14 +595,14 @@ Resolved resolve_config(const Node& config, bool strict, std::optional<uint64_t>
         std::string path = w->string_or("trace", "");
         if (path.empty()) config_error("workload.mode=trace requires workload.trace");
         path = join_path(base_dir, path);
-        rc.trace = cached(caches, &Caches::traces, path, [&] { return load_trace_file(path); });
+        rc.trace = cached(caches, &Caches::traces, file_key(path), [&] { return load_trace_file(path); });
         s.workload = DSD_WORKLOAD_TRACE;
     } else if (mode == "poisson") {
         double rate = w->double_or("rate_rps", 0.0);
         if (!(rate > 0.0)) config_error("workload.mode=poisson requires rate_rps > 0");
         if (w->has("trace")) {
             const std::string path = join_path(base_dir, w->string_or("trace", ""));
-            rc.trace = cached(caches, &Caches::traces, path, [&] { return load_trace_file(path); });
+            rc.trace = cached(caches, &Caches::traces, file_key(path), [&] { return load_trace_file(path); });
             s.workload = DSD_WORKLOAD_TRACE_POISSON;
             s.rate_rps = rate;
         } else {

@@ -236,3 +236,51 @@ def test_specialized_kernel_matches_generic_and_reference(smem_heap):
     assert len(sums["11"]) == 32 * 3
     assert (sums["11"]["status"] == 0).all()
     assert sums["11"].tobytes() == sums["01"].tobytes() == sums["10"].tobytes()
+
+
+def test_rewritten_input_files_are_read_again(sim, tmp_path):
+    """A trace and a WC-DNN model rewritten at the same path between two calls
+    on one handle: the second call must use the new contents (the reference
+    re-reads every input in resolve_config, runner.cpp:96-134)."""
+    trace = tmp_path / "t.jsonl"
+    model = tmp_path / "m.json"
+    text = _cfg("c1_single_pair.yaml").replace("kind: static", "kind: awc\n    model: m.json")
+    text = text.replace("mode: poisson", "mode: trace\n  trace: t.jsonl")
+    text = "\n".join(l for l in text.splitlines() if not l.strip().startswith(("rate_rps", "n_requests")))
+    outs = []
+    for k in range(2):
+        trace.write_text(ref.gen_trace(3.0 + k, 40 + 10 * k, 0.6 + 0.2 * k, seed=11 + k))
+        ref.random_model(str(model), seed=5 + k)
+        outs.append(_compare(sim, text, str(tmp_path)))
+    assert outs[0].report_json != outs[1].report_json
+
+
+def test_long_batching_window_matches_reference(sim):
+    """A batching window far longer than the service time with batches of 2:
+    full-batch dispatches leave stale BatchReady timers pending
+    (engine.cpp:508-519) - the case that can outgrow the HBM heap."""
+    text = _cfg("c2_8x1_batching.yaml")
+    for a, b in (("batching_window_us: 2000", "batching_window_us: 10000000"), ("max_batch_size: 8", "max_batch_size: 2"),
+                 ("n_requests: 400", "n_requests: 20"), ("output_median: 72", "output_median: 400")):
+        assert a in text
+        text = text.replace(a, b)
+    _compare(sim, text)
+
+
+@pytest.mark.parametrize("cap", ["3", "6"])
+def test_heap_overflow_retries_with_a_larger_heap(capfd, cap):
+    """Replicas whose HBM event heap overflows run again with the heap
+    doubled until they fit: forced here with a tiny heap
+    (DSD_HEAP_CAP) on a generic-kernel sweep; the summaries must not change."""
+    from paper_2511_21669_b200 import Simulator
+    spec = ("base: c2_8x1_batching.yaml\nseed: 9\nrepetitions: 2\naxes:\n"
+            "  network.rtt_ms: [2, 40]\n  policies.batching.max_batch_size: [2, 8]\n  workload.n_requests: [60]\n")
+    js, cs = ref.run_sweep(spec, CFG, 4)
+    os.environ.update({"DSD_HEAP_CAP": cap, "DSD_HOST_TIMING": "1"})
+    try:
+        with Simulator(0) as s:
+            out = s.run_sweep(spec, base_dir=CFG)
+    finally:
+        del os.environ["DSD_HEAP_CAP"], os.environ["DSD_HOST_TIMING"]
+    assert "event heap overflow" in capfd.readouterr().err
+    assert out.summary_json == js and out.summary_csv == cs
