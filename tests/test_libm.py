@@ -1,0 +1,30 @@
+"""Device transcendentals vs the host's glibc (VERDICT r1
+weak 1b).  k_stage evaluates the generator's log / cos / exp with CUDA libm
+while the reference uses glibc (proj/src/sim/rng.cpp:63-77): a 1-ulp
+difference changes an integer only at an exact .5 boundary of llround (a
+length, an arrival microsecond).  This checks >= 1e8 inputs per function from
+the generator's real argument domains (tests/native/libm_check.cu) and
+reports the bitwise mismatches and the integer flips they would cause."""
+import ctypes
+import json
+import os
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "native", "_build", "liblibm_check.so")
+N = int(os.environ.get("DSD_LIBM_N", str(10 ** 8)))
+
+
+@pytest.mark.parametrize("fn,name", [(0, "log(1-u)"), (1, "cos(2*pi*u)"), (2, "exp(mu+sigma*z)")])
+def test_device_libm_matches_glibc(fn, name):
+    L = ctypes.CDLL(LIB)
+    mm, flips, ex = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+    assert L.libm_check(fn, ctypes.c_uint64(12345), ctypes.c_int64(N), ctypes.byref(mm), ctypes.byref(flips),
+                        ctypes.byref(ex)) == 0
+    print(json.dumps({"function": name, "inputs": N, "bitwise_mismatches": mm.value, "integer_flips": flips.value,
+                      "example_input": ex.value if mm.value else None}))
+    # bitwise agreement needs glibc's algorithms on the device (not yet); what
+    # the engine consumes is the rounded integers, which must not move
+    assert flips.value == 0, f"{name}: {flips.value} of {N} inputs change an integer ({mm.value} differ bitwise)"
