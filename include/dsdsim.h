@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-#define DSD_ABI_VERSION 1
+#define DSD_ABI_VERSION 2
 
 #define DSD_OK 0
 #define DSD_ERR_CONFIG 2
@@ -176,7 +176,20 @@ typedef struct dsd_run_opts {
     int32_t collect_records; /* keep per-request records + sequences for dsd_fetch_records */
     int32_t feature_probe;   /* EngineOptions::feature_probe (engine.hpp:34): per-replica AWC
                                 feature sums, read back with dsd_batch_probe */
+    int32_t collect_event_log; /* EngineOptions::collect_event_log (engine.hpp:32-35): the
+                                  log_transition lines and RunResult::busy_intervals
+                                  (engine.cpp:213-219, 563-564), read back with
+                                  dsd_fetch_event_log; implies collect_records */
+    int32_t reserved;
 } dsd_run_opts;
+
+/* BusyInterval (proj/include/specsim/engine/engine.hpp:37-42). */
+typedef struct dsd_busy_interval {
+    int32_t role; /* 0 = target (Role::Target), 1 = draft */
+    int32_t server_id;
+    int64_t start_us;
+    int64_t end_us;
+} dsd_busy_interval;
 
 /* Per-replica result: RunResult scalars (engine.hpp:44-53), the SystemMetrics
  * fields that are not percentiles (metrics.hpp:38-47) and RunAggregates
@@ -241,6 +254,14 @@ int dsd_fetch_records(dsd_handle* h, size_t replica, dsd_request_record* records
                       int32_t* committed_seq, size_t seq_cap, int64_t* n_seq, int64_t* busy_us,
                       size_t busy_cap, char* err, size_t errlen);
 
+/* After a dsd_run_batch with collect_event_log: RunResult::event_log of one
+ * replica rendered exactly as the reference's log_transition lines, one per
+ * line with a trailing newline (what `specsim run --event-log` writes,
+ * tools/specsim_main.cpp:65-72; malloc'd, dsd_free), and its busy intervals
+ * in dispatch order (intervals[0..cap), *n_intervals = the count). */
+int dsd_fetch_event_log(dsd_handle* h, size_t replica, char** event_log, dsd_busy_interval* intervals,
+                        size_t cap, int64_t* n_intervals, char* err, size_t errlen);
+
 /* --- device-resident batch (for measurement: inputs stay in HBM) --------- */
 /* Uploads scenarios + replicas once; dsd_batch_launch then runs the kernels
  * asynchronously on the handle's stream with no host<->device traffic;
@@ -278,6 +299,14 @@ int dsd_run_simulation(dsd_handle* h, const char* config_yaml, const char* base_
                        int has_seed, uint64_t seed, char** report_json, char** report_csv,
                        uint64_t* events_processed, int64_t* end_time_us, double* agg,
                        char* err, size_t errlen);
+
+/* dsd_run_simulation with EngineOptions::collect_event_log: additionally the
+ * run's event log text and busy intervals (as dsd_fetch_event_log) - the
+ * `specsim run --event-log` path (tools/specsim_main.cpp:50-78). */
+int dsd_run_simulation_traced(dsd_handle* h, const char* config_yaml, const char* base_dir, int strict,
+                              int has_seed, uint64_t seed, char** report_json, char** event_log,
+                              dsd_busy_interval* intervals, size_t cap, int64_t* n_intervals,
+                              uint64_t* events_processed, char* err, size_t errlen);
 
 /* SweepSpec::from_node + run_sweep + sweep_summary_json/csv.  When out_dir is
  * non-empty the per-replica reports are written there with the reference's

@@ -232,6 +232,25 @@ int ref_run_config_full(const char* yaml_text, const char* base_dir, int has_see
     });
 }
 
+// RunResult::busy_intervals (engine.hpp:37-48, recorded at engine.cpp:563-564)
+// of one run as text, one interval per line: "<t|d> <server id> <start> <end>".
+int ref_run_config_busy(const char* yaml_text, const char* base_dir, int has_seed, std::uint64_t seed,
+                        char** busy, char* err, std::size_t errlen) {
+    return guarded(err, errlen, [&] {
+        yaml::Node cfg = yaml::parse_string(yaml_text);
+        ResolvedConfig rc =
+            resolve_config(cfg, true, has_seed ? std::optional<std::uint64_t>(seed) : std::nullopt,
+                           base_dir ? base_dir : ".");
+        SimulationOutput out = run_simulation(rc, EngineOptions{});
+        std::string text;
+        for (const auto& b : out.result.busy_intervals) {
+            text += b.role == Role::Target ? "t " : "d ";
+            text += std::to_string(b.server_id) + " " + std::to_string(b.start) + " " + std::to_string(b.end) + "\n";
+        }
+        *busy = dup_string(text);
+    });
+}
+
 // The stock run_sweep + sweep_summary_json/csv (sweep.cpp:87-199).
 int ref_run_sweep(const char* sweep_yaml, const char* base_dir, int parallel,
                   const char* out_dir, char** summary_json, char** summary_csv, char* err,

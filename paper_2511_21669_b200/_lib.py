@@ -51,6 +51,18 @@ class RequestRecord(ctypes.Structure):
     ]
 
 
+class BusyInterval(ctypes.Structure):
+    """dsd_busy_interval"""
+    _fields_ = [("role", ctypes.c_int32), ("server_id", ctypes.c_int32), ("start_us", ctypes.c_int64),
+                ("end_us", ctypes.c_int64)]
+
+
+class RunOpts(ctypes.Structure):
+    """dsd_run_opts"""
+    _fields_ = [("collect_records", ctypes.c_int32), ("feature_probe", ctypes.c_int32),
+                ("collect_event_log", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
 # Every symbol include/dsdsim.h declares (checked by tests/test_capi.py).
 EXPORTS = [
     "dsd_abi_version", "dsd_create", "dsd_create_devices", "dsd_device_count", "dsd_batch_shard_sizes",
@@ -62,7 +74,7 @@ EXPORTS = [
     "dsd_resolved_replica", "dsd_resolved_digest", "dsd_resolved_free", "dsd_plan_sweep",
     "dsd_sweep_plan_scenarios", "dsd_sweep_plan_replicas", "dsd_sweep_plan_origin", "dsd_sweep_plan_free", "dsd_emit_report",
     "dsd_sweep_point_seed", "dsd_free", "dsd_batch_probe", "dsd_build_scenarios", "dsd_generate_dataset",
-    "dsd_eval_policy",
+    "dsd_eval_policy", "dsd_fetch_event_log", "dsd_run_simulation_traced",
 ]
 DSD_PROBE_FIELDS = 8
 
@@ -107,6 +119,10 @@ def lib():
     L.dsd_last_transfer_bytes.argtypes = [vp, c.POINTER(c.c_int64), c.POINTER(c.c_int64)]
     L.dsd_run_simulation.argtypes = [vp, cp, cp, c.c_int, c.c_int, c.c_uint64, c.POINTER(vp), c.POINTER(vp),
                                      c.POINTER(c.c_uint64), c.POINTER(c.c_int64), c.POINTER(c.c_double), cp, sz]
+    L.dsd_fetch_event_log.argtypes = [vp, sz, c.POINTER(vp), c.POINTER(BusyInterval), sz, c.POINTER(c.c_int64), cp, sz]
+    L.dsd_run_simulation_traced.argtypes = [vp, cp, cp, c.c_int, c.c_int, c.c_uint64, c.POINTER(vp), c.POINTER(vp),
+                                            c.POINTER(BusyInterval), sz, c.POINTER(c.c_int64), c.POINTER(c.c_uint64),
+                                            cp, sz]
     L.dsd_run_sweep.argtypes = [vp, cp, cp, cp, c.POINTER(vp), c.POINTER(vp), c.POINTER(c.c_double), cp, sz]
     L.dsd_prepare_sweep.argtypes = [vp, cp, cp, c.c_int, c.c_int, c.POINTER(c.c_int64), c.POINTER(c.c_int64),
                                     cp, sz]

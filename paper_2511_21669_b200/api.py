@@ -148,6 +148,27 @@ class Simulator:
         return SimulationOutput(_take(rep) if report else None, _take(rcsv) if csv else None, ev.value, end.value,
                                 int(agg[0]), agg[1], agg[2], agg[3])
 
+    def run_simulation_traced(self, config: str, base_dir: Optional[str] = None, seed: Optional[int] = None,
+                              strict: bool = True):
+        """`specsim run --event-log`: (report_json, event_log text, busy intervals
+        [(role 't'|'d', server id, start_us, end_us)], events_processed) with
+        EngineOptions::collect_event_log (engine.hpp:32-35)."""
+        text, d = _text(config)
+        base_dir = base_dir or d or "."
+        c = ctypes
+        rep, log = c.c_void_p(), c.c_void_p()
+        n_iv, ev = c.c_int64(), c.c_uint64()
+        err = c.create_string_buffer(4096)
+        _check(self._L.dsd_run_simulation_traced(self._h, text.encode(), base_dir.encode(), int(strict),
+                                                 int(seed is not None), seed or 0, c.byref(rep), c.byref(log), None,
+                                                 0, c.byref(n_iv), c.byref(ev), err, 4096), err)
+        report, log_text = _take(rep), _take(log)
+        # the intervals from the same run (kept by the handle until the next batch)
+        buf = (_lib.BusyInterval * max(1, n_iv.value))()
+        _check(self._L.dsd_fetch_event_log(self._h, 0, None, buf, n_iv.value, c.byref(n_iv), err, 4096), err)
+        iv = [("d" if b.role else "t", b.server_id, b.start_us, b.end_us) for b in buf[:n_iv.value]]
+        return report, log_text, iv, ev.value
+
     def run_sweep(self, spec: str, base_dir: Optional[str] = None, out_dir: str = "") -> SweepOutput:
         text, d = _text(spec)
         base_dir = base_dir or d or "."

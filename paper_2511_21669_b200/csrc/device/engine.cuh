@@ -420,6 +420,34 @@ DSD_HD_NOINLINE void probe_iteration(const Workspace& W, int32_t rep, int64_t p,
     pr[7] += 1.0;
 }
 
+// EngineOptions::collect_event_log: one log_transition (engine.cpp:213-219)
+// and one busy interval (engine.cpp:563-564), appended to the replica's
+// region in event order; out of line - only logged runs take these calls.
+// A full region fails the replica like the sequence arena (kFailSeq).
+DSD_HD_NOINLINE int32_t elog_append(const Workspace& W, int32_t rep, int64_t now, int64_t i, uint32_t phase,
+                                    uint32_t detail, int32_t d, int32_t t) {
+    int64_t& n = W.elog_n[rep];
+    if (n >= W.elog_cap) return kFailSeq;
+    ElogRec& e = W.elog[static_cast<int64_t>(rep) * W.elog_cap + n++];
+    e.t = now;
+    e.req = static_cast<int32_t>(i);
+    e.draft = d;
+    e.target = t;
+    e.phase = static_cast<uint8_t>(phase);
+    e.detail = static_cast<uint8_t>(detail);
+    return kFailNone;
+}
+DSD_HD_NOINLINE int32_t busy_append(const Workspace& W, int32_t rep, int32_t server, int64_t start, int64_t end) {
+    int64_t& n = W.busy_n[rep];
+    if (n >= W.busy_cap) return kFailSeq;
+    BusyRec& b = W.busy_iv[static_cast<int64_t>(rep) * W.busy_cap + n++];
+    b.start = start;
+    b.end = end;
+    b.server = server;
+    b.pad = 0;
+    return kFailNone;
+}
+
 // ---------------------------------------------------------------------------
 // the engine
 //
@@ -595,6 +623,12 @@ struct Engine {
 #endif
     }
     DSD_HD bool collecting() const { return !spec && W.collect; }
+    // log_transition (engine.cpp:213-219) of request i, whose phase was just set
+    DSD_HD void log_tr(int64_t i, const ReqRec& r, uint32_t detail) {
+        if (spec || !W.elog) return;
+        const int32_t f = elog_append(W, rep, now, i, phase(r), detail, D > 0 ? r.drafter : -1, r.target);
+        if (f) fail = f;
+    }
     DSD_HD bool probing() const { return !spec && W.probe != nullptr; }
     DSD_HD bool fe() const { return pflags & 1u; }
     DSD_HD bool ps() const { return (pflags >> 1) & 1u; }
@@ -1062,6 +1096,10 @@ struct Engine {
         if (lat < 1) lat = 1;
         set_busy_flag(v, true);
         if (!is_draft) set_busy(v, get_busy(v) + lat);  // only target busy time is reported
+        if (!spec && W.elog) {
+            const int32_t f = busy_append(W, rep, is_draft ? ~(v - T) : v, now, now + lat);
+            if (f) fail = f;
+        }
         defer(now + lat, info(kEvComputeDone, 0, static_cast<uint32_t>(v)));
     }
 
@@ -1203,6 +1241,7 @@ struct Engine {
         int32_t t = route();
         r.target = t;
         ++SV(v_open, t);  // MetricsCollector::on_route
+        log_tr(i, r, kLogRouted);
         set_phase(r, kPhQueuedPrefill);
         if (fe()) {
             set_flag(r, kFused, true);
@@ -1266,6 +1305,7 @@ struct Engine {
             record_gamma(r, dec.gamma);
             r.pgamma = dec.gamma;
             set_phase(r, kPhSpeculating);
+            log_tr(i, r, kLogSpeculating);
             enqueue(T + d, i, 1, kOpDecode, dec.gamma, false);
         }
     }
@@ -1500,6 +1540,7 @@ struct Engine {
         r.done = now;
         if (r.first < 0) r.first = now;
         set_phase(r, kPhDone);
+        log_tr(i, r, kLogDone);
         const int32_t t = r.target;
         --SV(v_open, t);
         if (r.output >= 2 && ps()) {
@@ -1591,6 +1632,7 @@ struct Engine {
                 if (r.output > 0) defer(now, info(kEvIterStart, 0, static_cast<uint32_t>(i)));
             } else {  // send_proposal (engine.cpp:591-597)
                 set_phase(r, kPhInFlightToTarget);
+                log_tr(i, r, kLogProposalSent);
                 int64_t dl = net_delay(r.drafter, r.target);
                 r.outd = static_cast<int32_t>(dl);
                 defer(now + dl, info(kEvNetArrive, kMsgProposal, static_cast<uint32_t>(i)));
@@ -1614,6 +1656,7 @@ struct Engine {
             int64_t bd = net_delay(r.drafter, r.target);
             r.backd = static_cast<int32_t>(bd);
             set_phase(r, kPhInFlightToDraft);
+            log_tr(i, r, kLogVerifyDone);
             defer(now + bd, info(kEvNetArrive, kMsgResult, static_cast<uint32_t>(i)));
         } else {  // fused decode step: commit one token, then the next iteration
             if (commit_tokens(r, 1)) {
@@ -1641,6 +1684,10 @@ struct Engine {
         jitter.seed(seed, kLabelJitter);
         if (probing())
             for (int k = 0; k < kProbeFields; ++k) W.probe[static_cast<int64_t>(rep) * kProbeFields + k] = 0.0;
+        if (!spec && W.elog) {
+            W.elog_n[rep] = 0;
+            W.busy_n[rep] = 0;
+        }
         N = (S.workload == 0) ? S.n_requests : S.tr_n;
         seq_next = static_cast<uint32_t>(N);
         if (N > 0) next_arr_t = R[arrival_index(0)].arrival;
@@ -1804,6 +1851,7 @@ struct Engine {
         } else if (opaque(k) == kActNetProposal) {
             ReqRec& r = rec(arg);
             set_phase(r, kPhVerifying);
+            log_tr(arg, r, kLogProposalAtTarget);
             enqueue(r.target, arg, 1, kOpVerify, r.pgamma, true);
         } else if (opaque(k) == kActNetResult) {  // on_result_at_draft (engine.cpp:428-435)
             ReqRec& r = rec(arg);

@@ -117,6 +117,22 @@ struct DevSummary {  // == dsd_replica_summary
     int32_t has_duration, status;
 };
 
+// One log_transition line (engine.cpp:213-219), rendered on the host.
+enum : uint8_t { kLogRouted = 0, kLogSpeculating, kLogProposalSent, kLogProposalAtTarget, kLogVerifyDone, kLogDone };
+struct ElogRec {
+    int64_t t;
+    int32_t req, draft, target;
+    uint8_t phase, detail, pad[2];
+};
+static_assert(sizeof(ElogRec) == 24, "event-log record layout");
+// One BusyInterval (engine.hpp:37-42, engine.cpp:563-564): server = the
+// target index, or ~(draft index) for a draft server.
+struct BusyRec {
+    int64_t start, end;
+    int32_t server, pad;
+};
+static_assert(sizeof(BusyRec) == 24, "busy-interval record layout");
+
 struct DevRecord {  // == dsd_request_record
     int64_t drafter_id, prompt_length, output_length, arrival_us, first_token_us, completion_us,
         proposed, accepted;
@@ -215,6 +231,14 @@ struct Workspace {
     // pair {draft decode of gamma tokens at (1, c), verify at (gamma, c)} in
     // us - latency_us() of both queries, so looking one up is exact
     const int32_t* spec_lat;
+    // ---- event log + busy intervals (optional, EngineOptions::collect_event_log):
+    // per replica a region of elog_cap / busy_cap records at replica * cap,
+    // filled in event order; counts in elog_n / busy_n
+    ElogRec* elog;
+    BusyRec* busy_iv;
+    int64_t elog_cap, busy_cap;
+    int64_t* elog_n;
+    int64_t* busy_n;
     // ---- records (optional) ----
     int32_t collect;
     int64_t* rep_seqbase;  // [n] offset into the sequence arena

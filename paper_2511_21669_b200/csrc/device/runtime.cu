@@ -318,6 +318,8 @@ struct RuntimeImpl {
     cudaEvent_t ev[4] = {};
     DevBuf blob, scen, reps, arena, summary, fail, ltot, seqbase, seqg, seqc, rec, busy, ovf, probe, slat, sjobs;
     DevBuf heap2, ovf2;  // retry_heap_overflows: the larger event heap, its replica list
+    bool elog_on = false;  // the batch records the event log + busy intervals
+    DevBuf elog, busyiv, elogn;
     // shared-memory heap slots per replica for small topologies (0 = always
     // run the HBM variant; env DSD_SMEM_HEAP overrides, for tests)
     // 7: with 8 server fields x 2 servers and one session slot a warp needs
@@ -549,7 +551,7 @@ static int64_t spec_lat_jobs(Packed& P, std::vector<SpecLatJob>& jobs) {
 }
 
 void DeviceRuntime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n,
-                      bool collect, bool feature_probe) {
+                      bool collect, bool feature_probe, bool event_log) {
     RuntimeImpl& R = *impl_;
     DSD_CUDA(cudaSetDevice(R.device));
     R.prepared = false;
@@ -651,6 +653,8 @@ void DeviceRuntime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica
     // the lane placement is computed by launch() while k_stage runs
     R.place_pending = true;
     R.n = n;
+    R.elog_on = event_log;
+    collect = collect || event_log;  // the log's sizing uses the records' output totals
     R.collect = collect;
     if (collect) R.ltot.ensure(sizeof(int64_t) * std::max<size_t>(n, 1));
     lap("workspace");
@@ -760,6 +764,31 @@ void DeviceRuntime::launch() {
         R.W.seq_cap = acc;
         R.W.seq_gamma = static_cast<int32_t*>(R.seqg.p);
         R.W.seq_commit = static_cast<int32_t*>(R.seqc.p);
+        R.W.elog = nullptr;
+        R.W.busy_iv = nullptr;
+        if (R.elog_on) {
+            // every iteration commits >= 1 token, so a request logs at most
+            // 4 x output + 2 transitions and dispatches at most 2 x output + 2
+            // batch items
+            int64_t lmax = 0;
+            for (size_t i = 0; i < R.n; ++i) lmax = std::max(lmax, R.host_ltot[i]);
+            const int64_t ecap = 4 * lmax + 2 * R.W.c.nr + 16, bcap = 2 * lmax + 2 * R.W.c.nr + 16;
+            const size_t bytes = (sizeof(ElogRec) * ecap + sizeof(BusyRec) * bcap) * R.n;
+            size_t free_b = 0, total_b = 0;
+            DSD_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            if (bytes + (256u << 20) > free_b + R.elog.bytes + R.busyiv.bytes)
+                throw Error(DSD_ERR_RUNTIME, "event log of the batch (" + std::to_string(bytes >> 20) +
+                                                 " MiB) exceeds free device memory");
+            R.elog.ensure(sizeof(ElogRec) * ecap * R.n);
+            R.busyiv.ensure(sizeof(BusyRec) * bcap * R.n);
+            R.elogn.ensure(2 * sizeof(int64_t) * R.n);
+            R.W.elog = static_cast<ElogRec*>(R.elog.p);
+            R.W.busy_iv = static_cast<BusyRec*>(R.busyiv.p);
+            R.W.elog_cap = ecap;
+            R.W.busy_cap = bcap;
+            R.W.elog_n = static_cast<int64_t*>(R.elogn.p);
+            R.W.busy_n = R.W.elog_n + R.n;
+        }
     }
     if (R.step_stats) {
         R.stats.ensure((64 + 3 * R.n) * sizeof(unsigned long long));
@@ -972,6 +1001,28 @@ void DeviceRuntime::probe(double* out, size_t n) {
     if (n > R.n) n = R.n;
     sync();
     if (n) DSD_CUDA(cudaMemcpy(out, R.W.probe, sizeof(double) * kProbeFields * n, cudaMemcpyDeviceToHost));
+}
+
+void DeviceRuntime::fetch_event_log(size_t replica, std::vector<char>* elog, std::vector<char>* busy) {
+    RuntimeImpl& R = *impl_;
+    if (!R.ran || !R.elog_on) throw Error(DSD_ERR_RUNTIME, "the batch did not record an event log");
+    if (replica >= R.n) throw Error(DSD_ERR_RUNTIME, "replica index out of range");
+    sync();
+    int64_t n[2] = {0, 0};
+    DSD_CUDA(cudaMemcpy(&n[0], R.W.elog_n + replica, 8, cudaMemcpyDeviceToHost));
+    DSD_CUDA(cudaMemcpy(&n[1], R.W.busy_n + replica, 8, cudaMemcpyDeviceToHost));
+    if (elog) {
+        elog->resize(sizeof(ElogRec) * static_cast<size_t>(n[0]));
+        if (n[0])
+            DSD_CUDA(cudaMemcpy(elog->data(), R.W.elog + static_cast<int64_t>(replica) * R.W.elog_cap, elog->size(),
+                                cudaMemcpyDeviceToHost));
+    }
+    if (busy) {
+        busy->resize(sizeof(BusyRec) * static_cast<size_t>(n[1]));
+        if (n[1])
+            DSD_CUDA(cudaMemcpy(busy->data(), R.W.busy_iv + static_cast<int64_t>(replica) * R.W.busy_cap,
+                                busy->size(), cudaMemcpyDeviceToHost));
+    }
 }
 
 void DeviceRuntime::device_summaries(void** ptr, size_t* bytes) {

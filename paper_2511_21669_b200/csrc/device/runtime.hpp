@@ -33,7 +33,7 @@ public:
     // Packs + uploads scenarios and replicas and sizes the workspace.
     // feature_probe: accumulate the per-replica probe sums (probe()).
     void prepare(const dsd_scenario* scenarios, size_t n_scenarios, const dsd_replica* replicas,
-                 size_t n, bool collect_records, bool feature_probe = false);
+                 size_t n, bool collect_records, bool feature_probe = false, bool event_log = false);
     // Enqueues the staging + simulation kernels on the handle's stream.
     void launch();
     void sync();
@@ -47,6 +47,9 @@ public:
     void device_summaries(void** ptr, size_t* bytes);
     // After a probed run: [n][kProbeFields] sums per replica (see Workspace::probe).
     void probe(double* out, size_t n);
+    // After a run with event_log: the replica's log_transition records and
+    // busy intervals in event order (ElogRec / BusyRec, layout.cuh).
+    void fetch_event_log(size_t replica, std::vector<char>* elog, std::vector<char>* busy);
     void* stream();
     int device() const;
     int64_t last_launch_count() const;
@@ -73,7 +76,7 @@ public:
     Runtime& operator=(const Runtime&) = delete;
 
     void prepare(const dsd_scenario* scenarios, size_t n_scenarios, const dsd_replica* replicas,
-                 size_t n, bool collect_records, bool feature_probe = false);
+                 size_t n, bool collect_records, bool feature_probe = false, bool event_log = false);
     void launch();
     void sync();
     void summaries(dsd_replica_summary* out, size_t n);
@@ -84,6 +87,7 @@ public:
     // single-device handles only (the benchmark's NCCL gather reads it)
     void device_summaries(void** ptr, size_t* bytes);
     void probe(double* out, size_t n);
+    void fetch_event_log(size_t replica, std::vector<char>* elog, std::vector<char>* busy);
     void* stream();  // device 0's stream
     int64_t last_launch_count() const;        // summed over the devices
     void last_kernel_ms(double* sim_ms, double* gen_ms, double* total_ms);  // max over the devices

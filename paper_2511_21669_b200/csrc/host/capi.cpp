@@ -99,7 +99,8 @@ int dsd_run_batch(dsd_handle* h, const dsd_scenario* scenarios, size_t n_scenari
                   size_t n, const dsd_run_opts* opts, dsd_replica_summary* summaries, char* err, size_t errlen) {
     return guard(err, errlen, [&] {
         need(h);
-        h->rt->prepare(scenarios, n_scenarios, replicas, n, opts && opts->collect_records, opts && opts->feature_probe);
+        h->rt->prepare(scenarios, n_scenarios, replicas, n, opts && opts->collect_records, opts && opts->feature_probe,
+                       opts && opts->collect_event_log);
         h->rt->launch();
         h->rt->sync();
         if (summaries && n) h->rt->summaries(summaries, n);
@@ -120,7 +121,8 @@ int dsd_batch_prepare(dsd_handle* h, const dsd_scenario* scenarios, size_t n_sce
                       size_t n, const dsd_run_opts* opts, char* err, size_t errlen) {
     return guard(err, errlen, [&] {
         need(h);
-        h->rt->prepare(scenarios, n_scenarios, replicas, n, opts && opts->collect_records, opts && opts->feature_probe);
+        h->rt->prepare(scenarios, n_scenarios, replicas, n, opts && opts->collect_records, opts && opts->feature_probe,
+                       opts && opts->collect_event_log);
     });
 }
 
@@ -211,6 +213,63 @@ int dsd_run_simulation(dsd_handle* h, const char* config_yaml, const char* base_
             agg[2] = out.summary.mean_ttft_ms;
             agg[3] = out.summary.mean_tpot_ms;
         }
+    });
+}
+
+static void event_log_out(dsd::Runtime& rt, size_t replica, char** event_log, dsd_busy_interval* intervals,
+                          size_t cap, int64_t* n_intervals) {
+    std::vector<char> el, bi;
+    rt.fetch_event_log(replica, event_log ? &el : nullptr, (intervals || n_intervals) ? &bi : nullptr);
+    if (event_log) *event_log = dup(dsd::host::render_event_log(el));
+    if (intervals || n_intervals) {
+        const std::vector<dsd_busy_interval> iv = dsd::host::decode_busy_intervals(bi);
+        for (size_t k = 0; intervals && k < iv.size() && k < cap; ++k) intervals[k] = iv[k];
+        if (n_intervals) *n_intervals = static_cast<int64_t>(iv.size());
+    }
+}
+
+int dsd_fetch_event_log(dsd_handle* h, size_t replica, char** event_log, dsd_busy_interval* intervals, size_t cap,
+                        int64_t* n_intervals, char* err, size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        event_log_out(*h->rt, replica, event_log, intervals, cap, n_intervals);
+    });
+}
+
+int dsd_run_simulation_traced(dsd_handle* h, const char* config_yaml, const char* base_dir, int strict, int has_seed,
+                              uint64_t seed, char** report_json, char** event_log, dsd_busy_interval* intervals,
+                              size_t cap, int64_t* n_intervals, uint64_t* events_processed, char* err,
+                              size_t errlen) {
+    return guard(err, errlen, [&] {
+        need(h);
+        dsd::cfg::Node config = dsd::cfg::parse(config_yaml ? config_yaml : "");
+        dsd::host::Resolved rc =
+            dsd::host::resolve_config(config, strict != 0, has_seed ? std::optional<uint64_t>(seed) : std::nullopt,
+                                      base_dir ? base_dir : ".", &h->caches);
+        dsd_replica rep{};
+        rep.seed = rc.seed;
+        rep.gen_seed = rc.gen_seed;
+        h->rt->prepare(&rc.scen, 1, &rep, 1, true, false, true);
+        h->rt->launch();
+        h->rt->sync();
+        dsd::host::ReplicaOutput out;
+        h->rt->summaries(&out.summary, 1);
+        if (out.summary.status != DSD_OK)
+            throw dsd::Error(DSD_ERR_RUNTIME, "engine capacity exceeded on the device (event heap / sequence arena)");
+        if (report_json) {
+            int64_t nrec = 0, nseq = 0;
+            h->rt->fetch_records(0, nullptr, 0, &nrec, nullptr, nullptr, 0, &nseq, nullptr, 0);
+            out.records.resize(static_cast<size_t>(nrec));
+            out.gamma_seq.resize(static_cast<size_t>(nseq));
+            out.committed_seq.resize(static_cast<size_t>(nseq));
+            out.busy_us.resize(static_cast<size_t>(rc.scen.n_targets));
+            h->rt->fetch_records(0, out.records.data(), out.records.size(), &nrec, out.gamma_seq.data(),
+                                 out.committed_seq.data(), out.gamma_seq.size(), &nseq, out.busy_us.data(),
+                                 out.busy_us.size());
+            *report_json = dup(dsd::host::emit_report(out, rc.scen.n_targets, rc.digest, rc.seed));
+        }
+        event_log_out(*h->rt, 0, event_log, intervals, cap, n_intervals);
+        if (events_processed) *events_processed = out.summary.events_processed;
     });
 }
 

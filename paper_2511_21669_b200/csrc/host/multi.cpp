@@ -107,11 +107,11 @@ static void each_device(size_t n, F&& fn) {
 }
 
 void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n, bool collect,
-                      bool feature_probe) {
+                      bool feature_probe, bool event_log) {
     n_ = n;
     gathered_.clear();
     if (devs_.size() == 1) {
-        devs_[0]->prepare(sc, ns, reps, n, collect, feature_probe);
+        devs_[0]->prepare(sc, ns, reps, n, collect, feature_probe, event_log);
         return;
     }
     const size_t D = devs_.size();
@@ -126,7 +126,7 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
     each_device(D, [&](size_t d) {
         std::vector<dsd_replica> mine(global_of_[d].size());
         for (size_t j = 0; j < mine.size(); ++j) mine[j] = reps[global_of_[d][j]];
-        devs_[d]->prepare(sc, ns, mine.data(), mine.size(), collect, feature_probe);
+        devs_[d]->prepare(sc, ns, mine.data(), mine.size(), collect, feature_probe, event_log);
     });
 }
 
@@ -202,6 +202,15 @@ void Runtime::probe(double* out, size_t n) {
         const double* src = part[static_cast<size_t>(dev_of_[k])].data() + static_cast<size_t>(local_of_[k]) * DSD_PROBE_FIELDS;
         std::copy(src, src + DSD_PROBE_FIELDS, out + k * DSD_PROBE_FIELDS);
     }
+}
+
+void Runtime::fetch_event_log(size_t replica, std::vector<char>* elog, std::vector<char>* busy) {
+    if (devs_.size() == 1) {
+        devs_[0]->fetch_event_log(replica, elog, busy);
+        return;
+    }
+    if (replica >= n_) throw Error(DSD_ERR_RUNTIME, "replica index out of range");
+    devs_[static_cast<size_t>(dev_of_[replica])]->fetch_event_log(local_of_[replica], elog, busy);
 }
 
 void* Runtime::stream() { return devs_[0]->stream(); }

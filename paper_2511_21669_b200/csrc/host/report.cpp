@@ -1,6 +1,10 @@
 // report.cpp — byte-identical report emission (see report.hpp for citations).
 #include "report.hpp"
 
+#include <cstring>
+
+#include "../device/layout.cuh"
+
 #include <algorithm>
 #include <cmath>
 
@@ -248,6 +252,49 @@ std::string emit_report_csv(const ReplicaOutput& out) {
              std::to_string(r.n_iterations) + '\n';
     }
     return o;
+}
+
+std::string render_event_log(const std::vector<char>& bytes) {
+    // phase_name (engine.cpp:47-59) and the log_transition details
+    static const char* phases[] = {"arrived", "routed", "queued_prefill", "speculating",
+                                   "inflight_to_target", "verifying", "inflight_to_draft", "done"};
+    static const char* details[] = {"routed", "speculating", "proposal_sent", "proposal_at_target", "verify_done",
+                                    "done"};
+    const size_t n = bytes.size() / sizeof(ElogRec);
+    std::string out;
+    out.reserve(n * 72);
+    for (size_t k = 0; k < n; ++k) {
+        ElogRec e;
+        std::memcpy(&e, bytes.data() + k * sizeof(ElogRec), sizeof(e));
+        out += "t_us=";
+        out += std::to_string(e.t);
+        out += " req=";
+        out += std::to_string(e.req);
+        out += " phase=";
+        out += e.phase < 8 ? phases[e.phase] : "?";
+        out += " server=d";
+        out += std::to_string(e.draft);
+        out += "/t";
+        out += std::to_string(e.target);
+        out += ' ';
+        out += e.detail < 6 ? details[e.detail] : "?";
+        out += '\n';
+    }
+    return out;
+}
+
+std::vector<dsd_busy_interval> decode_busy_intervals(const std::vector<char>& bytes) {
+    const size_t n = bytes.size() / sizeof(BusyRec);
+    std::vector<dsd_busy_interval> out(n);
+    for (size_t k = 0; k < n; ++k) {
+        BusyRec b;
+        std::memcpy(&b, bytes.data() + k * sizeof(BusyRec), sizeof(b));
+        out[k].role = b.server < 0 ? 1 : 0;
+        out[k].server_id = b.server < 0 ? ~b.server : b.server;
+        out[k].start_us = b.start;
+        out[k].end_us = b.end;
+    }
+    return out;
 }
 
 }  // namespace dsd::host

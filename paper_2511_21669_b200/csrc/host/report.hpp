@@ -46,4 +46,10 @@ struct ReplicaOutput {
 std::string emit_report(const ReplicaOutput& r, int n_targets, const std::string& digest, uint64_t seed);
 std::string emit_report_csv(const ReplicaOutput& r);
 
+// RunResult::event_log (engine.cpp:213-219) from the device's ElogRec
+// records, one line each, newline-terminated (specsim_main.cpp:65-72).
+std::string render_event_log(const std::vector<char>& elog_records);
+// BusyRec records -> dsd_busy_interval (role, server id, start, end).
+std::vector<dsd_busy_interval> decode_busy_intervals(const std::vector<char>& busy_records);
+
 }  // namespace dsd::host

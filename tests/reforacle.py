@@ -40,6 +40,8 @@ def lib():
         L.ref_run_config_full.argtypes = [c.c_char_p, c.c_char_p, c.c_int, c.c_uint64, c.POINTER(c.c_void_p),
                                           c.POINTER(c.c_void_p), c.POINTER(c.c_void_p), c.POINTER(c.c_uint64),
                                           c.c_char_p, c.c_size_t]
+        L.ref_run_config_busy.argtypes = [c.c_char_p, c.c_char_p, c.c_int, c.c_uint64, c.POINTER(c.c_void_p),
+                                          c.c_char_p, c.c_size_t]
         L.ref_run_sweep.argtypes = [c.c_char_p, c.c_char_p, c.c_int, c.c_char_p, c.POINTER(c.c_void_p),
                                     c.POINTER(c.c_void_p), c.c_char_p, c.c_size_t]
         L.ref_sweep_point_seed.restype = c.c_uint64
@@ -97,6 +99,22 @@ def run_config(yaml_text, base_dir=".", seed=None, strict=True):
     if rc != 0:
         raise RefError(rc, err.value.decode())
     return _take(rep), ev.value, end.value, list(agg)
+
+
+def run_config_busy(yaml_text, base_dir=".", seed=None):
+    """RunResult::busy_intervals of one run: [(role 't'|'d', server id, start_us, end_us)]."""
+    c = ctypes
+    out = c.c_void_p()
+    err = c.create_string_buffer(4096)
+    rc = lib().ref_run_config_busy(yaml_text.encode(), base_dir.encode(), int(seed is not None), seed or 0,
+                                   c.byref(out), err, 4096)
+    if rc != 0:
+        raise RefError(rc, err.value.decode())
+    rows = []
+    for line in _take(out).splitlines():
+        r, i, a, b = line.split()
+        rows.append((r, int(i), int(a), int(b)))
+    return rows
 
 
 def run_config_full(yaml_text, base_dir=".", seed=None):

@@ -26,12 +26,14 @@ def test_library_exports_every_declared_symbol():
     L = _lib.lib()
     missing = [s for s in header_symbols() if not hasattr(L, s)]
     assert not missing
-    assert L.dsd_abi_version() == 1
+    assert L.dsd_abi_version() == 2
 
 
 def test_struct_sizes_match_header():
     assert ctypes.sizeof(_lib.ReplicaSummary) == 96
     assert ctypes.sizeof(_lib.RequestRecord) == 72
+    assert ctypes.sizeof(_lib.BusyInterval) == 24
+    assert ctypes.sizeof(_lib.RunOpts) == 16
 
 
 def _has_gpu():
