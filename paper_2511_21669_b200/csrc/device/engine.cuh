@@ -124,54 +124,53 @@ constexpr int32_t kSpecLatMax = 1 << 28;  // entries must stay below (32-bit rel
 // AWC: FeatureNormalizer::transform + WcDnn::forward (mlp.cpp:83-97,163-176)
 // with Backend::matvec in the AVX2 summation order the reference auto-selects
 // on AVX2 hosts (kernels_avx2.cpp:17-40, kernels_dispatch.cpp:21-26).
+//
+// The blob holds the network in a TRANSPOSED flat layout (pack.cpp,
+// awc_transpose): for each weight matrix, element (row r, column c) at
+// [c * rows + r], biases and the head as in the reference's layout
+// (mlp.cpp:20-48).  A warp evaluates a network cooperatively - lane l owns
+// output rows l, l + 32 - so at every step of a dot product the 32 lanes read
+// 32 consecutive weights (one 256-byte line, conflict-free in shared memory)
+// while the input element is a broadcast.  Each row is still summed in the
+// AVX2 order: 4 strided lane sums, (l0 + l2) + (l1 + l3), then the tail.
 // ---------------------------------------------------------------------------
-// one output row: 4 strided lane sums, hsum, scalar tail (the bias is added by the caller)
-DSD_HD double avx2_dot(const double* row, const double* x, int cols) {
+#ifndef DSD_AWC_FIXED
+#define DSD_AWC_FIXED 0
+#endif
+// one output row r of a transposed [cols][rows] matrix against x
+template <typename P>
+DSD_HD double avx2_dot_t(const P* wt, int rows, int r, const double* x, int cols) {
     const int tail = cols & ~3;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int c = 0;
     for (; c < tail; c += 4) {
-        a0 = a0 + row[c] * x[c];
-        a1 = a1 + row[c + 1] * x[c + 1];
-        a2 = a2 + row[c + 2] * x[c + 2];
-        a3 = a3 + row[c + 3] * x[c + 3];
+        a0 = a0 + wt[c * rows + r] * x[c];
+        a1 = a1 + wt[(c + 1) * rows + r] * x[c + 1];
+        a2 = a2 + wt[(c + 2) * rows + r] * x[c + 2];
+        a3 = a3 + wt[(c + 3) * rows + r] * x[c + 3];
     }
     double s = (a0 + a2) + (a1 + a3);  // hsum: lo+hi then unpackhi (kernels_avx2.cpp:17-23)
-    for (; c < cols; ++c) s += row[c] * x[c];
+    for (; c < cols; ++c) s += wt[c * rows + r] * x[c];
     return s;
 }
-
-// avx2_dot for a compile-time width: fully unrolled, so the row's weight
-// loads (read-only path) are scheduled ahead of the four add chains; the same
-// operations in the same order
-template <int C>
-DSD_HD double avx2_dot_fixed(const double* row, const double* x) {
-#ifdef __CUDA_ARCH__
-#define DSD_LDW(p) __ldg(p)
-#else
-#define DSD_LDW(p) (*(p))
-#endif
+// the same for compile-time widths (the trained shape): fully unrolled
+template <int R, int C>
+DSD_HD double avx2_dot_t_fixed(const double* wt, int r, const double* x) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
     for (int c = 0; c < (C & ~3); c += 4) {
-        a0 = a0 + DSD_LDW(row + c) * x[c];
-        a1 = a1 + DSD_LDW(row + c + 1) * x[c + 1];
-        a2 = a2 + DSD_LDW(row + c + 2) * x[c + 2];
-        a3 = a3 + DSD_LDW(row + c + 3) * x[c + 3];
+        a0 = a0 + wt[c * R + r] * x[c];
+        a1 = a1 + wt[(c + 1) * R + r] * x[c + 1];
+        a2 = a2 + wt[(c + 2) * R + r] * x[c + 2];
+        a3 = a3 + wt[(c + 3) * R + r] * x[c + 3];
     }
     double s = (a0 + a2) + (a1 + a3);
 #pragma unroll
-    for (int c = C & ~3; c < C; ++c) s += DSD_LDW(row + c) * x[c];
+    for (int c = C & ~3; c < C; ++c) s += wt[c * R + r] * x[c];
     return s;
-#undef DSD_LDW
 }
 // the WC-DNN shape the reference trains (TrainHyper: 5 features, 64 hidden)
 constexpr int kAwcH = 64, kAwcI = 5;
-
-DSD_HD void matvec_avx2_order(const double* w, const double* x, const double* bias, double* y,
-                              int rows, int cols) {
-    for (int r = 0; r < rows; ++r) y[r] = bias[r] + avx2_dot(w + static_cast<int64_t>(r) * cols, x, cols);
-}
 
 // FeatureNormalizer::transform (mlp.cpp:163-170): raw features -> model input
 DSD_HD void awc_normalize(const DevScenario& S, const double raw[5], double x[5]) {
@@ -181,9 +180,6 @@ DSD_HD void awc_normalize(const DevScenario& S, const double raw[5], double x[5]
         x[f] = span > 0.0 ? (v - S.awc_lo[f]) / span : 0.0;
     }
 }
-
-// WcDnn::forward (mlp.cpp:83-97) by one thread on a normalised input
-DSD_HD_NOINLINE double awc_forward_lane(const char* blob, const DevScenario& S, const double* x);
 
 // Per-warp scratch of the cooperative AWC evaluation (shared memory): the
 // requesting lanes' model inputs and results, the request flags, and the
@@ -196,71 +192,75 @@ struct AwcWarpScratch {
 };
 
 #ifdef __CUDACC__
-// WcDnn::forward (mlp.cpp:83-97) of one lane's request, evaluated by the whole
-// warp: each output row is one lane's avx2_dot in the reference's order, so
-// the result is bit-identical to awc_forward_lane; the vectors are broadcast
-// through shared memory.  Every lane of the warp must call it (converged).
-__device__ __noinline__ double awc_forward_warp(const char* blob, const DevScenario* S, const double* x,
-                                                AwcWarpScratch* sc) {
+// WcDnn::forward (mlp.cpp:83-97) of one network on a normalised input x,
+// evaluated by the whole warp from the transposed weights `pt` (shared
+// memory when the block staged them, else the blob); every lane of the warp
+// must call it (converged).  Returns the raw prediction on every lane.
+__device__ __forceinline__ double awc_forward_warp(const double* pt, const DevScenario* S, const double* x,
+                                                   AwcWarpScratch* sc) {
     const int lane = threadIdx.x & (kLanes - 1);
     const int H = S->awc_hidden, I = S->awc_input;
-    const double* p = blob_ptr<double>(blob, S->o_awc_params);
-    if (H == kAwcH && I == kAwcI) {  // compile-time widths (the trained shape)
+    if (DSD_AWC_FIXED && H == kAwcH && I == kAwcI) {  // compile-time widths (the trained shape)
         constexpr int FH = kAwcH, FI = kAwcI;
-        for (int r = lane; r < FH; r += kLanes) sc->hv[r] = p[FH * FI + r] + avx2_dot_fixed<FI>(p + r * FI, x);
+#pragma unroll
+        for (int k = 0; k < FH / kLanes; ++k) {
+            const int r = lane + k * kLanes;
+            sc->hv[r] = pt[FH * FI + r] + avx2_dot_t_fixed<FH, FI>(pt, r, x);
+        }
         __syncwarp();
-        int64_t off = FH * FI + FH;
+        int off = FH * FI + FH;
         for (int b = 0; b < S->awc_blocks; ++b) {
-            const double* w1 = p + off;
+            const double* w1 = pt + off;
             const double* b1 = w1 + FH * FH;
             const double* w2 = b1 + FH;
             const double* b2 = w2 + FH * FH;
 #pragma unroll
             for (int k = 0; k < FH / kLanes; ++k) {
                 const int r = lane + k * kLanes;
-                const double u = b1[r] + avx2_dot_fixed<FH>(w1 + r * FH, sc->hv);
-                const double sg = 1.0 / (1.0 + exp(-u));
+                const double u = b1[r] + avx2_dot_t_fixed<FH, FH>(w1, r, sc->hv);
+                const double sg = 1.0 / (1.0 + exp(-u));  // kernels::silu (kernels_scalar.cpp:65-70)
                 sc->sv[r] = u * sg;
             }
             __syncwarp();
+            // (the products read sv; each lane updates only its own rows of hv)
 #pragma unroll
             for (int k = 0; k < FH / kLanes; ++k) {
                 const int r = lane + k * kLanes;
-                sc->hv[r] += b2[r] + avx2_dot_fixed<FH>(w2 + r * FH, sc->sv);
+                sc->hv[r] += b2[r] + avx2_dot_t_fixed<FH, FH>(w2, r, sc->sv);
             }
             __syncwarp();
             off += 2 * FH * FH + 2 * FH;
         }
         double out = 0.0;
         if (lane == 0) {
-            const double* w_out = p + off;
-            out = w_out[FH];
+            const double* w_out = pt + off;
+            out = w_out[FH];  // b_out, then the sequential head (mlp.cpp:93-95)
             for (int i = 0; i < FH; ++i) out += w_out[i] * sc->hv[i];
         }
         __syncwarp();
         return __shfl_sync(0xffffffffu, out, 0);
     }
-    for (int r = lane; r < H; r += kLanes) sc->hv[r] = p[H * I + r] + avx2_dot(p + static_cast<int64_t>(r) * I, x, I);
+    for (int r = lane; r < H; r += kLanes) sc->hv[r] = pt[H * I + r] + avx2_dot_t(pt, H, r, x, I);
     __syncwarp();
-    int64_t off = static_cast<int64_t>(H) * I + H;
+    int off = H * I + H;
     for (int b = 0; b < S->awc_blocks; ++b) {
-        const double* w1 = p + off;
-        const double* b1 = w1 + static_cast<int64_t>(H) * H;
+        const double* w1 = pt + off;
+        const double* b1 = w1 + H * H;
         const double* w2 = b1 + H;
-        const double* b2 = w2 + static_cast<int64_t>(H) * H;
+        const double* b2 = w2 + H * H;
         for (int r = lane; r < H; r += kLanes) {
-            const double u = b1[r] + avx2_dot(w1 + static_cast<int64_t>(r) * H, sc->hv, H);
+            const double u = b1[r] + avx2_dot_t(w1, H, r, sc->hv, H);
             const double sg = 1.0 / (1.0 + exp(-u));  // kernels::silu (kernels_scalar.cpp:65-70)
             sc->sv[r] = u * sg;
         }
         __syncwarp();
-        for (int r = lane; r < H; r += kLanes) sc->hv[r] += b2[r] + avx2_dot(w2 + static_cast<int64_t>(r) * H, sc->sv, H);
+        for (int r = lane; r < H; r += kLanes) sc->hv[r] += b2[r] + avx2_dot_t(w2, H, r, sc->sv, H);
         __syncwarp();
-        off += 2 * static_cast<int64_t>(H) * H + 2 * H;
+        off += 2 * H * H + 2 * H;
     }
     double out = 0.0;
     if (lane == 0) {
-        const double* w_out = p + off;
+        const double* w_out = pt + off;
         out = w_out[H];  // b_out, then the sequential head (mlp.cpp:93-95)
         for (int i = 0; i < H; ++i) out += w_out[i] * sc->hv[i];
     }
@@ -268,28 +268,21 @@ __device__ __noinline__ double awc_forward_warp(const char* blob, const DevScena
     return __shfl_sync(0xffffffffu, out, 0);
 }
 
-// Serves every pending AWC request of the warp.  A few requests (a sparse or
-// single-replica batch) are evaluated one at a time by all 32 lanes (idle and
-// finished lanes included); many requests at once are faster as one
-// evaluation per requesting lane, in parallel.
-constexpr int kAwcCoopMax = 6;
-__device__ __forceinline__ void awc_serve_warp(const char* blob, const DevScenario* my_scen, AwcWarpScratch* sc) {
+// Serves every pending AWC request of the warp: one network at a time, each
+// evaluated by all 32 lanes (idle and finished lanes included).  `staged`:
+// the block's shared-memory copy of the weights at blob offset staged_off
+// (or null); other models are read from the blob.
+__device__ __forceinline__ void awc_serve_warp(const char* blob, const DevScenario* my_scen, AwcWarpScratch* sc,
+                                               const double* staged, int64_t staged_off) {
     const int lane = threadIdx.x & (kLanes - 1);
     unsigned pending = __ballot_sync(0xffffffffu, sc->req[lane] != 0);
-    if (__popc(pending) > kAwcCoopMax) {
-        if (sc->req[lane]) {
-            sc->raw[lane] = awc_forward_lane(blob, *my_scen, sc->x[lane]);
-            sc->req[lane] = 0;
-        }
-        __syncwarp();
-        return;
-    }
     while (pending) {
         const int src = __ffs(pending) - 1;
         pending &= pending - 1;
         const DevScenario* S = reinterpret_cast<const DevScenario*>(
             __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(my_scen), src));
-        const double raw = awc_forward_warp(blob, S, sc->x[src], sc);
+        const double* pt = S->o_awc_params == staged_off && staged ? staged : blob_ptr<double>(blob, S->o_awc_params);
+        const double raw = awc_forward_warp(pt, S, sc->x[src], sc);
         if (lane == src) {
             sc->raw[lane] = raw;
             sc->req[lane] = 0;
@@ -298,57 +291,6 @@ __device__ __forceinline__ void awc_serve_warp(const char* blob, const DevScenar
     }
 }
 #endif
-
-// WcDnn::forward (mlp.cpp:83-97) by one thread on a normalised input
-DSD_HD_NOINLINE double awc_forward_lane(const char* blob, const DevScenario& S, const double* x) {
-    const int H = S.awc_hidden, I = S.awc_input;
-    const double* p = blob_ptr<double>(blob, S.o_awc_params);
-    if (H == kAwcH && I == kAwcI) {  // compile-time widths (the trained shape)
-        constexpr int FH = kAwcH, FI = kAwcI;
-        double h[FH], s[FH];
-        for (int r = 0; r < FH; ++r) h[r] = p[FH * FI + r] + avx2_dot_fixed<FI>(p + r * FI, x);
-        int64_t off = FH * FI + FH;
-        for (int b = 0; b < S.awc_blocks; ++b) {
-            const double* w1 = p + off;
-            const double* b1 = w1 + FH * FH;
-            const double* w2 = b1 + FH;
-            const double* b2 = w2 + FH * FH;
-            for (int r = 0; r < FH; ++r) {
-                const double u = b1[r] + avx2_dot_fixed<FH>(w1 + r * FH, h);
-                const double sg = 1.0 / (1.0 + exp(-u));  // kernels::silu (kernels_scalar.cpp:65-70)
-                s[r] = u * sg;
-            }
-            for (int r = 0; r < FH; ++r) h[r] += b2[r] + avx2_dot_fixed<FH>(w2 + r * FH, s);
-            off += 2 * FH * FH + 2 * FH;
-        }
-        const double* w_out = p + off;
-        double out = w_out[FH];
-        for (int i = 0; i < FH; ++i) out += w_out[i] * h[i];
-        return out;
-    }
-    double h[kMaxHidden], u[kMaxHidden], s[kMaxHidden];
-    int64_t off = 0;
-    matvec_avx2_order(p + off, x, p + off + H * I, h, H, I);
-    off += static_cast<int64_t>(H) * I + H;
-    for (int b = 0; b < S.awc_blocks; ++b) {
-        const double* w1 = p + off;
-        const double* b1 = w1 + static_cast<int64_t>(H) * H;
-        const double* w2 = b1 + H;
-        const double* b2 = w2 + static_cast<int64_t>(H) * H;
-        matvec_avx2_order(w1, h, b1, u, H, H);
-        for (int i = 0; i < H; ++i) {  // kernels::silu (kernels_scalar.cpp:65-70)
-            double sg = 1.0 / (1.0 + exp(-u[i]));
-            s[i] = u[i] * sg;
-        }
-        matvec_avx2_order(w2, s, b2, u, H, H);
-        for (int i = 0; i < H; ++i) h[i] += u[i];
-        off += 2 * static_cast<int64_t>(H) * H + 2 * H;
-    }
-    const double* w_out = p + off;
-    double out = w_out[H];  // b_out
-    for (int i = 0; i < H; ++i) out += w_out[i] * h[i];
-    return out;
-}
 
 // ---------------------------------------------------------------------------
 // pair / target metric rings (MetricsCollector, metrics.cpp:40-128) and the
@@ -1270,10 +1212,12 @@ struct Engine {
                 // evaluates the network cooperatively (awc_serve_warp) before
                 // the continuation kActBeginAwc runs the smoother and the rest
                 const int32_t t = r.target;
-                double f[5];
-                extract_features(W, rep, pair_of(d, t), t, SV(v_open, t), S.queue_capacity, link(d, t).rtt_ms, f);
+                // (the raw features go straight into the lane's shared-memory
+                // input slot and are normalised in place: no local array)
                 const int lane = hw_lane();
-                awc_normalize(S, f, awc->x[lane]);
+                double* xin = awc->x[lane];
+                extract_features(W, rep, pair_of(d, t), t, SV(v_open, t), S.queue_capacity, link(d, t).rtt_ms, xin);
+                awc_normalize(S, xin, xin);
                 awc->req[lane] = 1;
                 push_act(act(kActBeginAwc, static_cast<uint32_t>(i)));
                 return;

@@ -222,6 +222,11 @@ struct Workspace {
     // ... and per replica [n][3]: vote rounds it ran in, session-loop
     // iterations (builds with -DDSD_REP_STATS), cycles from init to finish
     unsigned long long* rep_stats;
+    // AWC batches: blob offset / double count of the one WC-DNN (transposed
+    // layout) the kAwc blocks stage into shared memory, or -1
+    int64_t awc_stage_off;
+    int32_t awc_stage_n;
+    int32_t pad_awc;
     // specialised kernel: run the active session's speculation loop directly
     // (Engine::session_run); env DSD_SESSION_FAST=0 disables it
     int32_t session_fast;

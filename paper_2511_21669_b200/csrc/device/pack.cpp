@@ -37,9 +37,48 @@ struct BlobBuilder {
         if (dedupe && src) seen[src] = static_cast<int64_t>(off);
         return static_cast<int64_t>(off);
     }
+    // a derived array (e.g. a re-laid-out copy) stored once per source `key`
+    int64_t put_keyed(const void* key, const std::vector<double>& v) {
+        auto it = seen.find(key);
+        if (it != seen.end()) return it->second;
+        const int64_t off = put(v.data(), sizeof(double) * v.size(), false);
+        seen[key] = off;
+        return off;
+    }
 };
 
 [[noreturn]] void cfg_error(const std::string& m) { throw Error(DSD_ERR_CONFIG, m); }
+
+int64_t awc_param_count(const dsd_awc_model& m);
+
+// WcDnn parameters (the reference's flat layout, mlp.cpp:20-48) in the
+// device's transposed layout: every weight matrix [rows][cols] stored as
+// [cols][rows] (engine.cuh, awc_forward_warp); biases and the head as is.
+std::vector<double> awc_transpose(const dsd_awc_model& m) {
+    const int64_t H = m.hidden, I = m.input;
+    std::vector<double> t(static_cast<size_t>(awc_param_count(m)));
+    const double* p = m.params;
+    int64_t o = 0;
+    auto mat = [&](int64_t rows, int64_t cols) {
+        for (int64_t r = 0; r < rows; ++r)
+            for (int64_t c = 0; c < cols; ++c) t[static_cast<size_t>(o + c * rows + r)] = p[o + r * cols + c];
+        o += rows * cols;
+    };
+    auto vec = [&](int64_t n) {
+        for (int64_t k = 0; k < n; ++k) t[static_cast<size_t>(o + k)] = p[o + k];
+        o += n;
+    };
+    mat(H, I);
+    vec(H);
+    for (int b = 0; b < m.blocks; ++b) {
+        mat(H, H);
+        vec(H);
+        mat(H, H);
+        vec(H);
+    }
+    vec(H + 1);
+    return t;
+}
 
 int64_t awc_param_count(const dsd_awc_model& m) {
     int64_t H = m.hidden, I = m.input;
@@ -238,7 +277,7 @@ void pack_batch_into(Packed& P, const dsd_scenario* sc, size_t ns, const dsd_rep
             d.awc_hidden = m.hidden;
             d.awc_blocks = m.blocks;
             d.awc_input = m.input;
-            d.o_awc_params = B.put(m.params, sizeof(double) * awc_param_count(m));
+            d.o_awc_params = B.put_keyed(m.params, awc_transpose(m));
             for (int f = 0; f < 5; ++f) {
                 d.awc_lo[f] = m.norm_lo[f];
                 d.awc_hi[f] = m.norm_hi[f];

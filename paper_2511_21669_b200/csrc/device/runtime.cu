@@ -129,10 +129,13 @@ __device__ __forceinline__ uint32_t vote_kind(unsigned best) {
 // other instantiations compile that code out.
 // kSpecLimit: overflow limit of the specialised action stack (1 only in the
 // test instantiation that forces the HBM re-run, DSD_SPEC_STACK_LIMIT=1).
+// kAwc kernels run with blocks of up to kAwcMaxThreads threads: one block
+// per SM shares one shared-memory copy of the WC-DNN weights (staging).
+constexpr int kAwcMaxThreads = 512;
 template <bool kSmem, bool kStats, bool kSpec = false, bool kAwc = false, int kSpecLimit = kSpecStack>
-__global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_BLOCKS) k_simulate(const __grid_constant__ Workspace W,
-                                                                      const int32_t* list, const int32_t* count,
-                                                     int32_t smem_heap_cap) {
+__global__ void __launch_bounds__(kAwc ? kAwcMaxThreads : kBlock,
+                                  kAwc ? 1 : (kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_BLOCKS))
+    k_simulate(const __grid_constant__ Workspace W, const int32_t* list, const int32_t* count, int32_t smem_heap_cap) {
     int64_t rep = 0;
     const bool live = replica_of(W, list, count, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x, rep);
     const int64_t r = live ? rep : 0;
@@ -143,7 +146,21 @@ __global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_
     int32_t nsc;
     unsigned char* hot = nullptr;
     AwcWarpScratch* awc = nullptr;
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem_all[];
+    // AWC batches whose scenarios share one model: the block stages its
+    // (transposed) weights into shared memory once; the per-warp regions follow
+    const double* awc_w = nullptr;
+    unsigned char* smem = smem_all;
+    if constexpr (kAwc) {
+        if (W.awc_stage_off >= 0) {
+            double* sw = reinterpret_cast<double*>(smem_all);
+            const double* gw = reinterpret_cast<const double*>(W.blob + W.awc_stage_off);
+            for (int32_t k = threadIdx.x; k < W.awc_stage_n; k += blockDim.x) sw[k] = gw[k];
+            __syncthreads();
+            awc_w = sw;
+            smem = smem_all + ((static_cast<int64_t>(W.awc_stage_n) * 8 + 127) & ~int64_t(127));
+        }
+    }
     if constexpr (kSmem) {
         const int lane = threadIdx.x % kLanes;
         nsc = kSpec ? 2 : static_cast<int32_t>(W.c.ns);
@@ -183,7 +200,7 @@ __global__ void __launch_bounds__(kBlock, kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_
     for (;;) {
         // AWC decisions requested during the last chains: the whole warp
         // evaluates each requester's network (warp-uniform branch)
-        if constexpr (kAwc) awc_serve_warp(W.blob, &e.S, awc);
+        if constexpr (kAwc) awc_serve_warp(W.blob, &e.S, awc, awc_w, W.awc_stage_off);
         // the kind most lanes have pending (majority vote)
         const unsigned peers = __match_any_sync(0xffffffffu, kind);
         const unsigned score = kind == kActNone ? 0u : vote_score(static_cast<unsigned>(__popc(peers)), kind);
@@ -319,6 +336,12 @@ struct RuntimeImpl {
     DevBuf blob, scen, reps, arena, summary, fail, ltot, seqbase, seqg, seqc, rec, busy, ovf, probe, slat, sjobs;
     DevBuf heap2, ovf2;  // retry_heap_overflows: the larger event heap, its replica list
     bool elog_on = false;  // the batch records the event log + busy intervals
+    // AWC batches with one shared model: warps per block of the kAwc kernels
+    // (0: weights not staged, blocks of kBlock threads) for the
+    // shared-memory and the HBM variant; staged weight bytes (128-aligned)
+    int awc_warps_smem = 0, awc_warps_hbm = 0;
+    size_t awc_wbytes = 0;
+    int smem_optin = 0;
     DevBuf elog, busyiv, elogn;
     // shared-memory heap slots per replica for small topologies (0 = always
     // run the HBM variant; env DSD_SMEM_HEAP overrides, for tests)
@@ -356,6 +379,7 @@ struct RuntimeImpl {
     int64_t h2d_bytes = 0, d2h_bytes = 0;
     bool spec_stack_limit1 = false;  // DSD_SPEC_STACK_LIMIT=1 (tests: force the HBM re-run)
     bool session_fast = true;        // Engine::session_run in the specialised kernel (DSD_SESSION_FAST=0: off)
+    bool awc_stage = true;           // stage one shared WC-DNN per block in shared memory (DSD_AWC_STAGE=0: off)
     bool smem_launch = false;
     void* pinned = nullptr;  // host_summaries() buffer (page-locked)
     bool pinned_valid = false;  // it holds the last launch's summaries
@@ -367,6 +391,20 @@ struct RuntimeImpl {
     std::vector<int64_t> h_busy;
     std::vector<int32_t> h_seqg, h_seqc;
 };
+
+// Block shape of the HBM variant's launches: the AWC scratch per warp (and
+// the staged weights) or nothing.
+struct HbmCfg {
+    unsigned threads;
+    size_t smem;
+};
+static HbmCfg hbm_cfg(const RuntimeImpl& R) {
+    if (!R.W.c.awc) return {static_cast<unsigned>(kBlock), 0};
+    if (R.awc_warps_hbm > 0)
+        return {static_cast<unsigned>(R.awc_warps_hbm * kLanes),
+                R.awc_wbytes + static_cast<size_t>(R.awc_warps_hbm) * sizeof(AwcWarpScratch)};
+    return {static_cast<unsigned>(kBlock), (kBlock / kLanes) * sizeof(AwcWarpScratch)};
+}
 
 DeviceRuntime::DeviceRuntime(int device) : impl_(new RuntimeImpl) {
     int count = 0;
@@ -386,6 +424,7 @@ DeviceRuntime::DeviceRuntime(int device) : impl_(new RuntimeImpl) {
     if (const char* s = std::getenv("DSD_SPEC_STACK_LIMIT")) impl_->spec_stack_limit1 = std::atoi(s) == 1;
     if (const char* s = std::getenv("DSD_SPECIALIZE")) impl_->specialize = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_SESSION_FAST")) impl_->session_fast = std::atoi(s) != 0;
+    if (const char* s = std::getenv("DSD_AWC_STAGE")) impl_->awc_stage = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_PLACEMENT")) impl_->placement = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_SPREAD")) impl_->spread = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_SPREAD_MAX")) impl_->spread_max = std::atof(s);
@@ -398,6 +437,7 @@ DeviceRuntime::DeviceRuntime(int device) : impl_(new RuntimeImpl) {
     }
     DSD_CUDA(cudaDeviceGetAttribute(&impl_->sms, cudaDevAttrMultiProcessorCount, device));
     DSD_CUDA(cudaDeviceGetAttribute(&impl_->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device));
+    DSD_CUDA(cudaDeviceGetAttribute(&impl_->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     for (auto& ev : impl_->ev) DSD_CUDA(cudaEventCreate(&ev));
 }
 
@@ -627,6 +667,43 @@ void DeviceRuntime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica
     W.fail = static_cast<int32_t*>(R.fail.p);
     W.collect = collect ? 1 : 0;
     W.session_fast = R.session_fast ? 1 : 0;
+    // AWC: stage the WC-DNN into shared memory when every AWC scenario of the
+    // batch uses one model and it fits next to at least one warp's state
+    W.awc_stage_off = -1;
+    W.awc_stage_n = 0;
+    R.awc_warps_smem = R.awc_warps_hbm = 0;
+    R.awc_wbytes = 0;
+    if (c.awc && R.awc_stage) {
+        int64_t off = -1, cnt = 0;
+        bool one = true;
+        for (const DevScenario& d : P.scen) {
+            if (d.window_kind != 2 || d.fused_everything) continue;
+            const int64_t k = static_cast<int64_t>(d.awc_hidden) * d.awc_input + d.awc_hidden +
+                              static_cast<int64_t>(d.awc_blocks) * (2 * d.awc_hidden * d.awc_hidden + 2 * d.awc_hidden) +
+                              d.awc_hidden + 1;
+            if (off < 0) {
+                off = d.o_awc_params;
+                cnt = k;
+            } else if (d.o_awc_params != off) {
+                one = false;
+            }
+        }
+        const size_t wb = (static_cast<size_t>(cnt) * 8 + 127) & ~size_t(127);
+        // (the kernels' static shared memory - the step-stats counters - comes off the opt-in limit)
+        const int64_t room = static_cast<int64_t>(R.smem_optin) - 1024 - static_cast<int64_t>(wb);
+        if (one && off >= 0 && room > 0) {
+            const int64_t sw = static_cast<int64_t>(smem_warp_bytes(c.ns <= kSmemServers ? c.ns : 2, R.smem_heap, true));
+            R.awc_warps_hbm = static_cast<int>(std::min<int64_t>(16, room / static_cast<int64_t>(sizeof(AwcWarpScratch))));
+            R.awc_warps_smem = c.ns <= kSmemServers && R.smem_heap > 0 ? static_cast<int>(std::min<int64_t>(16, room / sw)) : 0;
+            if (R.awc_warps_hbm > 0 && (R.awc_warps_smem > 0 || !(c.ns <= kSmemServers && R.smem_heap > 0))) {
+                W.awc_stage_off = off;
+                W.awc_stage_n = static_cast<int32_t>(cnt);
+                R.awc_wbytes = wb;
+            } else {
+                R.awc_warps_hbm = R.awc_warps_smem = 0;
+            }
+        }
+    }
     if (feature_probe) {
         R.probe.ensure(sizeof(double) * kProbeFields * std::max<size_t>(n, 1));
         W.probe = static_cast<double*>(R.probe.p);
@@ -680,7 +757,9 @@ static void place_lanes(RuntimeImpl& R) {
                                                                   R.W.c.awc != 0);
         per_sm = std::max<int64_t>(1, std::min<int64_t>(max_blocks, R.smem_per_sm / (bytes + 1024)));
     }
-    const int64_t warp_cap = R.sms * per_sm * (kBlock / kLanes);
+    int64_t warp_cap = R.sms * per_sm * (kBlock / kLanes);
+    if (R.W.c.awc && (R.W.c.ns <= kSmemServers && R.smem_heap > 0 ? R.awc_warps_smem : R.awc_warps_hbm) > 0)
+        warp_cap = R.sms * (R.W.c.ns <= kSmemServers && R.smem_heap > 0 ? R.awc_warps_smem : R.awc_warps_hbm);
     std::vector<int32_t> pl = placement_list(R.packed, n, warp_cap);
     if (!pl.empty() && R.placement && R.lanes_per_warp == kLanes) {
         R.place.ensure(4 * pl.size());
@@ -725,20 +804,31 @@ void DeviceRuntime::launch() {
         return;
     }
     const unsigned grid = static_cast<unsigned>((R.n + kBlock - 1) / kBlock);
-    // the HBM variant's only shared memory: the cooperative AWC scratch; its
-    // carveout keeps just that (the rest of the array is L1, which holds the
-    // AWC weights and the replicas' state)
-    const size_t hbm_smem = R.W.c.awc ? (kBlock / kLanes) * sizeof(AwcWarpScratch) : 0;
+    // the HBM variant's only shared memory: the cooperative AWC scratch (and
+    // the staged AWC weights); its carveout keeps just that (the rest of the
+    // array is L1, which holds the replicas' state)
+    const HbmCfg hcfg = hbm_cfg(R);
+    const size_t hbm_smem = hcfg.smem;
+    auto hgrid_of = [&](int64_t threads) { return static_cast<unsigned>((threads + hcfg.threads - 1) / hcfg.threads); };
     // sized for the blocks a launch of `g` blocks puts on an SM
     auto hbm_carveout = [&](unsigned g) {
         if (R.carveout >= 0) return;
-        const int64_t per_sm = std::min<int64_t>(DSD_MIN_BLOCKS, (g + R.sms - 1) / R.sms);
+        const int64_t per_sm = R.awc_warps_hbm > 0 ? 1 : std::min<int64_t>(DSD_MIN_BLOCKS, (g + R.sms - 1) / R.sms);
         const int64_t need = hbm_smem ? per_sm * (static_cast<int64_t>(hbm_smem) + 1024) : 0;
         const int pct = static_cast<int>(std::min<int64_t>(100, (100 * need + R.smem_per_sm - 1) / R.smem_per_sm));
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<false, false, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     };
-    hbm_carveout(grid);
+    if (R.W.c.awc) {
+        for (auto k : {k_simulate<false, false, false, true>, k_simulate<false, true, false, true>,
+                       k_simulate<true, false, false, true>, k_simulate<true, true, false, true>}) {
+            cudaFuncAttributes fa;
+            DSD_CUDA(cudaFuncGetAttributes(&fa, k));
+            DSD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          R.smem_optin - static_cast<int>(fa.sharedSizeBytes)));
+        }
+    }
+    hbm_carveout(hgrid_of(static_cast<int64_t>(R.n)));
     DSD_CUDA(cudaEventRecord(R.ev[0], R.stream));
     k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, R.collect ? static_cast<int64_t*>(R.ltot.p) : nullptr, nullptr,
                                            nullptr);
@@ -800,10 +890,13 @@ void DeviceRuntime::launch() {
     const bool smem = R.W.c.ns <= kSmemServers && R.smem_heap > 0;
     R.smem_launch = smem;
     if (smem) {
-        const size_t bytes = static_cast<size_t>(kBlock / kLanes) * smem_warp_bytes(R.W.c.ns, R.smem_heap, R.W.c.awc != 0);
+        // AWC with staged weights: one block of awc_warps_smem warps per SM
+        const unsigned sthreads = R.awc_warps_smem > 0 ? static_cast<unsigned>(R.awc_warps_smem * kLanes) : kBlock;
+        const size_t bytes = (R.awc_warps_smem > 0 ? R.awc_wbytes : 0) +
+                             static_cast<size_t>(sthreads / kLanes) * smem_warp_bytes(R.W.c.ns, R.smem_heap, R.W.c.awc != 0);
         const int32_t* pcount = R.place_n ? static_cast<const int32_t*>(R.place.p) : nullptr;
         const int32_t* plist = R.place_n ? pcount + 1 : nullptr;
-        const unsigned sgrid = R.place_n ? static_cast<unsigned>((R.place_n + kBlock - 1) / kBlock) : grid;
+        const unsigned sgrid = static_cast<unsigned>(((R.place_n ? R.place_n : static_cast<int64_t>(R.n)) + sthreads - 1) / sthreads);
         const bool spec = R.spec_ok && R.specialize && !R.collect && !R.W.probe;
         // Carveout: just the shared memory of the blocks one wave puts on an
         // SM (1 KB of it reserved per block); the rest of the 256 KB array is
@@ -811,7 +904,7 @@ void DeviceRuntime::launch() {
         // blocks) even when 65,536 replicas need 7 per SM, costing 32-64 KB of L1.
         int pct = R.carveout;
         if (pct < 0) {
-            const int64_t per_sm = std::min<int64_t>(spec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_BLOCKS, (sgrid + R.sms - 1) / R.sms);
+            const int64_t per_sm = R.awc_warps_smem > 0 ? 1 : std::min<int64_t>(spec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_BLOCKS, (sgrid + R.sms - 1) / R.sms);
             const int64_t need = per_sm * (static_cast<int64_t>(bytes) + 1024);
             pct = static_cast<int>(std::min<int64_t>(100, (100 * need + R.smem_per_sm - 1) / R.smem_per_sm));
         }
@@ -828,7 +921,7 @@ void DeviceRuntime::launch() {
             (R.step_stats ? k_simulate<true, true, true> : k_simulate<true, false, true>)<<<sgrid, kBlock, bytes, R.stream>>>(
                 R.W, plist, pcount, R.smem_heap);
         else if (R.W.c.awc)
-            (R.step_stats ? k_simulate<true, true, false, true> : k_simulate<true, false, false, true>)<<<sgrid, kBlock, bytes,
+            (R.step_stats ? k_simulate<true, true, false, true> : k_simulate<true, false, false, true>)<<<sgrid, sthreads, bytes,
                                                                                                     R.stream>>>(
                 R.W, plist, pcount, R.smem_heap);
         else
@@ -845,17 +938,17 @@ void DeviceRuntime::launch() {
         k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, R.collect ? static_cast<int64_t*>(R.ltot.p) : nullptr, list,
                                                 count);
         (R.W.c.awc ? (R.step_stats ? k_simulate<false, true, false, true> : k_simulate<false, false, false, true>)
-                    : (R.step_stats ? k_simulate<false, true> : k_simulate<false, false>))<<<grid, kBlock, hbm_smem, R.stream>>>(R.W, list, count, 0);
+                    : (R.step_stats ? k_simulate<false, true> : k_simulate<false, false>))<<<hgrid_of(static_cast<int64_t>(R.n)), hcfg.threads, hbm_smem, R.stream>>>(R.W, list, count, 0);
         DSD_CUDA(cudaGetLastError());
         R.launches += 4;
     } else {
         // (HBM state is indexed by replica, so a lane placement is just a thread -> replica list)
         const int32_t* pcount = R.place_n ? static_cast<const int32_t*>(R.place.p) : nullptr;
         const int32_t* plist = R.place_n ? pcount + 1 : nullptr;
-        const unsigned hgrid = R.place_n ? static_cast<unsigned>((R.place_n + kBlock - 1) / kBlock) : grid;
-        if (hgrid != grid) hbm_carveout(hgrid);
+        const unsigned hgrid = hgrid_of(R.place_n ? R.place_n : static_cast<int64_t>(R.n));
+        hbm_carveout(hgrid);
         (R.W.c.awc ? (R.step_stats ? k_simulate<false, true, false, true> : k_simulate<false, false, false, true>)
-                    : (R.step_stats ? k_simulate<false, true> : k_simulate<false, false>))<<<hgrid, kBlock, hbm_smem, R.stream>>>(R.W, plist, pcount, 0);
+                    : (R.step_stats ? k_simulate<false, true> : k_simulate<false, false>))<<<hgrid, hcfg.threads, hbm_smem, R.stream>>>(R.W, plist, pcount, 0);
         DSD_CUDA(cudaGetLastError());
         ++R.launches;
     }
@@ -900,10 +993,11 @@ static void retry_heap_overflows(RuntimeImpl& R) {
         W2.c.hc = hc;
         W2.h_time = static_cast<int64_t*>(R.heap2.p);
         W2.h_key = reinterpret_cast<uint64_t*>(W2.h_time + slots);
-        const size_t hbm_smem = R.W.c.awc ? (kBlock / kLanes) * sizeof(AwcWarpScratch) : 0;
+        const HbmCfg hc_cfg = hbm_cfg(R);
         k_stage<<<grid, kBlock, 0, R.stream>>>(W2, nullptr, list, count);
-        (R.W.c.awc ? k_simulate<false, false, false, true> : k_simulate<false, false>)<<<grid, kBlock, hbm_smem,
-                                                                                           R.stream>>>(W2, list, count, 0);
+        (R.W.c.awc ? k_simulate<false, false, false, true> : k_simulate<false, false>)<<<
+            static_cast<unsigned>((R.n + hc_cfg.threads - 1) / hc_cfg.threads), hc_cfg.threads, hc_cfg.smem,
+            R.stream>>>(W2, list, count, 0);
         DSD_CUDA(cudaGetLastError());
         R.launches += 3;
     }
