@@ -1315,33 +1315,45 @@ struct Engine {
         int32_t nw = 0;  // verifies dispatched (net_wait_count; their wait is 0)
         uint32_t seq = seq_next;
         int32_t t2 = 0;  // proposal arrival of the last iteration (verify enqueue time)
-        int2 l;
+        int2 l = lat[prompt + tokens];
         int a_acc, a_cons;
+        int32_t ncur;
         bool full;
         for (;;) {
-            l = lat[prompt + tokens];
             // consume_acceptance (engine.cpp:17-32) at the cursor: the run of
-            // trailing ones of the g bits there, capped at g (bit g forced)
-            if (cur + g <= nb) {
+            // ones of the g bits there (cyclic over the request's nb bits),
+            // capped at g - trailing ones of a 64-bit window with bit g forced
+            {
                 const int sh = cur & 63;
-                const uint64_t w = (w0 >> sh) | ((w1 << 1) << (63 - sh));
+                uint64_t w = (w0 >> sh) | ((w1 << 1) << (63 - sh));  // bits cur.. (0 past the request's words)
+                const int32_t n1 = nb - cur;                          // bits left before the wrap
+                if (n1 < g) {
+                    // the window wraps once (nb >= g): the request's first
+                    // bits follow its last ones
+                    if (nb >= g) {
+                        w = (w & ((1ull << n1) - 1)) | (bits[0] << n1);
+                    } else {  // shorter than the window: several wraps, bit by bit
+                        uint64_t x = 0;
+                        for (int32_t k = 0, c = cur; k < g; ++k, c = c + 1 == nb ? 0 : c + 1)
+                            x |= ((bits[c >> 6] >> (c & 63)) & 1u) << k;
+                        w = x;
+                    }
+                }
 #ifdef __CUDA_ARCH__
                 a_acc = __ffsll(static_cast<long long>(~w | (1ull << g))) - 1;
 #else
                 a_acc = __builtin_ctzll(~w | (1ull << g));
 #endif
                 a_cons = a_acc < g ? a_acc + 1 : g;
-            } else {  // the window wraps past the request's last bit
-                a_acc = 0;
-                a_cons = 0;
-                int32_t c = cur;
-                while (a_cons < g) {
-                    const uint64_t bb = (bits[c >> 6] >> (c & 63)) & 1u;
-                    c = c + 1 == nb ? 0 : c + 1;
-                    ++a_cons;
-                    if (bb) ++a_acc; else break;
-                }
+                ncur = cur + a_cons;
+                while (ncur >= nb) ncur -= nb;  // (cursor + consumed) mod nbits
             }
+            // the next iteration's context, and its latency pair loaded now so
+            // the load overlaps this iteration's time checks
+            const int32_t remaining = output - tokens;
+            const int32_t committed = a_acc + 1 < remaining ? a_acc + 1 : remaining;
+            const int32_t ntok = tokens + committed;
+            const int2 lnext = ntok < output ? lat[prompt + ntok] : l;
             // IterationStart -> draft done -> proposal -> verify done -> result
             const int32_t t4 = nr + l.x + lk + l.y + lk;
             full = target_ok && t4 < xr;
@@ -1352,8 +1364,6 @@ struct Engine {
             ++ng;
             ++nw;
             busy0 += l.y;
-            int32_t ncur = cur + a_cons;
-            ncur = ncur == nb ? 0 : ncur;
             if ((ncur >> 6) != (cur >> 6)) {  // the cursor moved to another word
                 const int32_t wi = ncur >> 6;
                 w0 = wi == (cur >> 6) + 1 ? w1 : bits[wi];
@@ -1363,8 +1373,8 @@ struct Engine {
             lcr = a_acc + 1;
             prop += a_cons;
             acc += a_acc;
-            const int32_t remaining = output - tokens;
-            tokens += lcr < remaining ? lcr : remaining;
+            tokens = ntok;
+            l = lnext;
             ++nc;
             if (first < 0) first = base + nr;
             seq += 4;
@@ -1411,8 +1421,6 @@ struct Engine {
                 seq += 3;
                 ++nw;
                 busy0 += l.y;
-                int32_t ncur = cur + a_cons;
-                ncur = ncur == nb ? 0 : ncur;
                 if ((ncur >> 6) != (cur >> 6)) w0 = bits[ncur >> 6];
                 cur = ncur;
                 lcr = a_acc + 1;
