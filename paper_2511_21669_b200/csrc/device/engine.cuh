@@ -218,7 +218,7 @@ __device__ __forceinline__ double awc_forward_warp(const double* pt, const DevSc
             for (int k = 0; k < FH / kLanes; ++k) {
                 const int r = lane + k * kLanes;
                 const double u = b1[r] + avx2_dot_t_fixed<FH, FH>(w1, r, sc->hv);
-                const double sg = 1.0 / (1.0 + exp(-u));  // kernels::silu (kernels_scalar.cpp:65-70)
+                const double sg = 1.0 / (1.0 + DSD_EXP(-u));  // kernels::silu (kernels_scalar.cpp:65-70)
                 sc->sv[r] = u * sg;
             }
             __syncwarp();
@@ -250,7 +250,7 @@ __device__ __forceinline__ double awc_forward_warp(const double* pt, const DevSc
         const double* b2 = w2 + H * H;
         for (int r = lane; r < H; r += kLanes) {
             const double u = b1[r] + avx2_dot_t(w1, H, r, sc->hv, H);
-            const double sg = 1.0 / (1.0 + exp(-u));  // kernels::silu (kernels_scalar.cpp:65-70)
+            const double sg = 1.0 / (1.0 + DSD_EXP(-u));  // kernels::silu (kernels_scalar.cpp:65-70)
             sc->sv[r] = u * sg;
         }
         __syncwarp();

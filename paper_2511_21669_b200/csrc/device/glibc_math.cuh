@@ -1,0 +1,178 @@
+// glibc_math.cuh — glibc 2.39's exp() and log() restated for the device, so
+// the workload generator (proj/src/sim/rng.cpp:63-77: exponential gaps,
+// lognormal lengths) and the AWC SiLU (proj/src/awc/kernels_scalar.cpp:65-70)
+// round exactly as the reference does on its x86-64 host.
+//
+// glibc takes both from ARM's optimized-routines (sysdeps/ieee754/dbl-64/
+// e_exp.c, e_log.c): a 128-entry table + short polynomial.  On x86-64 with
+// FMA (the GPU box's Xeon, and this container's) libm's ifunc selects the
+// variants compiled with -mfma, where GCC contracts every a + b*c whose
+// product has one use into fma(b, c, a) and e_log.c takes its
+// __FP_FAST_FMA branch; the evaluation below spells those fmas out in the
+// same places.  The tables are glibc's own data (glibc_tables.inc, extracted
+// from libm by tools/gen_glibc_tables.py); tests/test_glibc_math.py checks
+// them and both functions against the host's exp / log bit for bit (CPU),
+// and tests/test_libm.py the device results on 1e8 generator inputs.
+#pragma once
+#include <cstdint>
+#include <cstring>
+
+#ifdef __CUDACC__
+#define DSD_GLIBC_CONST __device__ static const
+#define DSD_GLIBC_FN __device__ __forceinline__
+#else
+#define DSD_GLIBC_CONST static const
+#define DSD_GLIBC_FN inline
+#include <cmath>
+#endif
+
+namespace dsd {
+namespace glibc {
+
+#include "glibc_tables.inc"
+
+DSD_GLIBC_FN double as_double(uint64_t u) {
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double(static_cast<long long>(u));
+#else
+    double d;
+    std::memcpy(&d, &u, 8);
+    return d;
+#endif
+}
+DSD_GLIBC_FN uint64_t as_u64(double d) {
+#ifdef __CUDA_ARCH__
+    return static_cast<uint64_t>(__double_as_longlong(d));
+#else
+    uint64_t u;
+    std::memcpy(&u, &d, 8);
+    return u;
+#endif
+}
+DSD_GLIBC_FN double fma_(double a, double b, double c) {
+#ifdef __CUDA_ARCH__
+    return __fma_rn(a, b, c);
+#else
+    return std::fma(a, b, c);
+#endif
+}
+
+// e_exp.c specialcase(): |x| near the overflow / underflow limits
+DSD_GLIBC_FN double exp_special(double tmp, uint64_t sbits, uint64_t ki) {
+    if ((ki & 0x80000000u) == 0) {
+        // k > 0: the exponent of scale might have overflowed by <= 460
+        sbits -= 1009ull << 52;
+        const double scale = as_double(sbits);
+        return 0x1p1009 * fma_(scale, tmp, scale);
+    }
+    // k < 0: care in the subnormal range.  scale * tmp has two uses here
+    // (y and lo), so GCC computes it once and fuses neither addition.
+    sbits += 1022ull << 52;
+    const double scale = as_double(sbits);
+    const double st = scale * tmp;
+    double y = scale + st;
+    if (y < 1.0) {
+        // round y to the right precision before scaling into the subnormal
+        // range (lo + hi exactly represents scale + scale * tmp)
+        const double lo = scale - y + st;
+        double hi = 1.0 + y;
+        double lo2 = 1.0 - hi + y + lo;
+        y = (hi + lo2) - 1.0;
+        if (y == 0.0) y = 0.0;  // (the sign of a zero result)
+    }
+    return 0x1p-1022 * y;
+}
+
+// __exp (glibc 2.39 e_exp.c, FMA variant)
+DSD_GLIBC_FN double exp(double x) {
+    const uint64_t ux = as_u64(x);
+    uint32_t abstop = static_cast<uint32_t>(ux >> 52) & 0x7ff;
+    // top12(0x1p-54) = 0x3c9, top12(512.0) = 0x408, top12(1024.0) = 0x409
+    if (abstop - 0x3c9u >= 0x408u - 0x3c9u) {
+        if (abstop - 0x3c9u >= 0x80000000u) return 1.0 + x;  // tiny x (WANT_ROUNDING)
+        if (abstop >= 0x409u) {
+            if (ux == 0xfff0000000000000ull) return 0.0;  // -inf
+            if (abstop >= 0x7ffu) return 1.0 + x;     // inf / nan
+            return (ux >> 63) ? 0x1p-767 * 0x1p-767 : 0x1p769 * 0x1p769;  // __math_uflow / __math_oflow
+        }
+        abstop = 0;  // large |x|: specialcase below
+    }
+    const double InvLn2N = kExpHead[0], Shift = kExpHead[1], NegLn2hiN = kExpHead[2], NegLn2loN = kExpHead[3];
+    const double C2 = kExpHead[4], C3 = kExpHead[5], C4 = kExpHead[6], C5 = kExpHead[7];
+    // z = InvLn2N * x; kd = z + Shift - the product's one use is that sum
+    double kd = fma_(InvLn2N, x, Shift);
+    const uint64_t ki = as_u64(kd);
+    kd -= Shift;
+    const double r = fma_(kd, NegLn2loN, fma_(kd, NegLn2hiN, x));  // x + kd*NegLn2hiN + kd*NegLn2loN
+    const uint64_t idx = 2 * (ki % 128);
+    const uint64_t top = ki << (52 - 7);
+    const double tail = as_double(kExpTab[idx]);
+    const uint64_t sbits = kExpTab[idx + 1] + top;
+    const double r2 = r * r;
+    // tail + r + r2 * (C2 + r * C3) + r2 * r2 * (C4 + r * C5)
+    const double tmp = fma_(r2 * r2, fma_(r, C5, C4), fma_(r2, fma_(r, C3, C2), tail + r));
+    if (abstop == 0) return exp_special(tmp, sbits, ki);
+    const double scale = as_double(sbits);
+    return fma_(scale, tmp, scale);  // scale + scale * tmp
+}
+
+// __log (glibc 2.39 e_log.c, FMA variant)
+DSD_GLIBC_FN double log(double x) {
+    uint64_t ix = as_u64(x);
+    const uint32_t top = static_cast<uint32_t>(ix >> 48);
+    const uint64_t LO = 0x3fee000000000000ull;  // asuint64(1.0 - 0x1p-4)
+    const uint64_t HI = 0x3ff1090000000000ull;  // asuint64(1.0 + 0x1.09p-4)
+    const double* A = kLogHead + 2;
+    const double* B = kLogHead + 7;
+    if (ix - LO < HI - LO) {
+        // close to 1.0
+        if (ix == 0x3ff0000000000000ull) return 0;
+        const double r = x - 1.0;
+        const double r2 = r * r;
+        const double r3 = r * r2;
+        // r3 * (B1 + r*B2 + r2*B3 + r3*(B4 + r*B5 + r2*B6 + r3*(B7 + r*B8 + r2*B9 + r3*B10)))
+        const double q3 = fma_(r3, B[10], fma_(r2, B[9], fma_(r, B[8], B[7])));
+        const double q2 = fma_(r3, q3, fma_(r2, B[6], fma_(r, B[5], B[4])));
+        const double q1 = fma_(r3, q2, fma_(r2, B[3], fma_(r, B[2], B[1])));
+        // y = r3 * q1, then y += lo: the product's one use is that sum
+        double w = r * 0x1p27;
+        const double rhi = r + w - w;
+        const double rlo = r - rhi;
+        w = rhi * rhi * B[0];  // B[0] == -0.5
+        const double hi = r + w;
+        double lo = r - hi + w;
+        lo = fma_(B[0] * rlo, rhi + r, lo);  // lo += B[0] * rlo * (rhi + r)
+        double y = fma_(r3, q1, lo);         // y = r3 * q1; y += lo
+        y += hi;
+        return y;
+    }
+    if (top - 0x0010u >= 0x7ff0u - 0x0010u) {
+        // x < 0x1p-1022 or inf or nan
+        if (ix * 2 == 0) return -1.0 / 0.0;                    // __math_divzero(1)
+        if (ix == 0x7ff0000000000000ull) return x;             // log(inf) == inf
+        if ((top & 0x8000u) || (top & 0x7ff0u) == 0x7ff0u) return (x - x) / (x - x);  // __math_invalid
+        ix = as_u64(x * 0x1p52);  // subnormal: normalise
+        ix -= 52ull << 52;
+    }
+    const uint64_t OFF = 0x3fe6000000000000ull;
+    const uint64_t tmp = ix - OFF;
+    const int i = static_cast<int>((tmp >> (52 - 7)) % 128);
+    const int k = static_cast<int>(static_cast<int64_t>(tmp) >> 52);
+    const uint64_t iz = ix - (tmp & (0xfffull << 52));
+    const double invc = kLogTab[2 * i], logc = kLogTab[2 * i + 1];
+    const double z = as_double(iz);
+    const double r = fma_(z, invc, -1.0);  // __FP_FAST_FMA branch
+    const double kd = static_cast<double>(k);
+    const double Ln2hi = kLogHead[0], Ln2lo = kLogHead[1];
+    const double w = fma_(kd, Ln2hi, logc);              // kd * Ln2hi + logc
+    const double hi = w + r;
+    const double lo = fma_(kd, Ln2lo, w - hi + r);       // w - hi + r + kd * Ln2lo
+    const double r2 = r * r;
+    // lo + r2 * A[0] + r * r2 * (A[1] + r * A[2] + r2 * (A[3] + r * A[4])) + hi
+    const double p = fma_(r2, fma_(r, A[4], A[3]), fma_(r, A[2], A[1]));
+    const double y = fma_(r * r2, p, fma_(r2, A[0], lo)) + hi;
+    return y;
+}
+
+}  // namespace glibc
+}  // namespace dsd

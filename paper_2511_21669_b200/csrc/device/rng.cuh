@@ -15,6 +15,18 @@
 #define DSD_HD_NOINLINE
 #endif
 
+#include "glibc_math.cuh"
+
+// exp / log as the reference's x86-64 glibc computes them: glibc's own
+// algorithms on the device (glibc_math.cuh), the host's libm on the host
+#ifdef __CUDA_ARCH__
+#define DSD_EXP(x) ::dsd::glibc::exp(x)
+#define DSD_LOG(x) ::dsd::glibc::log(x)
+#else
+#define DSD_EXP(x) std::exp(x)
+#define DSD_LOG(x) std::log(x)
+#endif
+
 namespace dsd {
 
 // fnv1a64 (fnv.hpp:10-18); constexpr so stream labels hash at compile time.
@@ -85,16 +97,16 @@ struct Rng {
     DSD_HD double uniform(double lo, double hi) { return lo + (hi - lo) * unit(); }
 
     // exponential (rng.cpp:68-71)
-    DSD_HD double exponential(double mean) { return -mean * log(1.0 - unit()); }
+    DSD_HD double exponential(double mean) { return -mean * DSD_LOG(1.0 - unit()); }
 
     // normal / lognormal (rng.cpp:73-83): Box-Muller, exactly two draws
     DSD_HD double normal(double mean, double stddev) {
         double u1 = 1.0 - unit();
         double u2 = unit();
-        double z = sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+        double z = sqrt(-2.0 * DSD_LOG(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
         return mean + stddev * z;
     }
-    DSD_HD double lognormal(double mu, double sigma) { return exp(normal(mu, sigma)); }
+    DSD_HD double lognormal(double mu, double sigma) { return DSD_EXP(normal(mu, sigma)); }
 };
 
 }  // namespace dsd

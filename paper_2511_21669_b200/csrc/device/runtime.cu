@@ -398,11 +398,19 @@ struct HbmCfg {
     unsigned threads;
     size_t smem;
 };
-static HbmCfg hbm_cfg(const RuntimeImpl& R) {
+// Warps per staged-AWC block for a launch of `threads` threads: at most
+// `cap`, but few enough that the blocks cover every SM (one block per SM
+// fits next to the staged weights).
+static int awc_block_warps(const RuntimeImpl& R, int cap, int64_t threads) {
+    const int64_t warps = (threads + kLanes - 1) / kLanes;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cap, (warps + R.sms - 1) / R.sms)));
+}
+static HbmCfg hbm_cfg(const RuntimeImpl& R, int64_t threads) {
     if (!R.W.c.awc) return {static_cast<unsigned>(kBlock), 0};
-    if (R.awc_warps_hbm > 0)
-        return {static_cast<unsigned>(R.awc_warps_hbm * kLanes),
-                R.awc_wbytes + static_cast<size_t>(R.awc_warps_hbm) * sizeof(AwcWarpScratch)};
+    if (R.awc_warps_hbm > 0) {
+        const int w = awc_block_warps(R, R.awc_warps_hbm, threads);
+        return {static_cast<unsigned>(w * kLanes), R.awc_wbytes + static_cast<size_t>(w) * sizeof(AwcWarpScratch)};
+    }
     return {static_cast<unsigned>(kBlock), (kBlock / kLanes) * sizeof(AwcWarpScratch)};
 }
 
@@ -804,10 +812,26 @@ void DeviceRuntime::launch() {
         return;
     }
     const unsigned grid = static_cast<unsigned>((R.n + kBlock - 1) / kBlock);
+    if (R.W.c.awc) {
+        for (auto k : {k_simulate<false, false, false, true>, k_simulate<false, true, false, true>,
+                       k_simulate<true, false, false, true>, k_simulate<true, true, false, true>}) {
+            cudaFuncAttributes fa;
+            DSD_CUDA(cudaFuncGetAttributes(&fa, k));
+            DSD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          R.smem_optin - static_cast<int>(fa.sharedSizeBytes)));
+        }
+    }
+    DSD_CUDA(cudaEventRecord(R.ev[0], R.stream));
+    k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, R.collect ? static_cast<int64_t*>(R.ltot.p) : nullptr, nullptr,
+                                           nullptr);
+    DSD_CUDA(cudaGetLastError());
+    ++R.launches;
+    if (R.place_pending) place_lanes(R);
     // the HBM variant's only shared memory: the cooperative AWC scratch (and
     // the staged AWC weights); its carveout keeps just that (the rest of the
     // array is L1, which holds the replicas' state)
-    const HbmCfg hcfg = hbm_cfg(R);
+    // (the block shape of the HBM variant's main launch: the placement's thread count)
+    const HbmCfg hcfg = hbm_cfg(R, R.place_n ? R.place_n : static_cast<int64_t>(R.n));
     const size_t hbm_smem = hcfg.smem;
     auto hgrid_of = [&](int64_t threads) { return static_cast<unsigned>((threads + hcfg.threads - 1) / hcfg.threads); };
     // sized for the blocks a launch of `g` blocks puts on an SM
@@ -819,22 +843,7 @@ void DeviceRuntime::launch() {
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
         DSD_CUDA(cudaFuncSetAttribute(k_simulate<false, false, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     };
-    if (R.W.c.awc) {
-        for (auto k : {k_simulate<false, false, false, true>, k_simulate<false, true, false, true>,
-                       k_simulate<true, false, false, true>, k_simulate<true, true, false, true>}) {
-            cudaFuncAttributes fa;
-            DSD_CUDA(cudaFuncGetAttributes(&fa, k));
-            DSD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          R.smem_optin - static_cast<int>(fa.sharedSizeBytes)));
-        }
-    }
-    hbm_carveout(hgrid_of(static_cast<int64_t>(R.n)));
-    DSD_CUDA(cudaEventRecord(R.ev[0], R.stream));
-    k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, R.collect ? static_cast<int64_t*>(R.ltot.p) : nullptr, nullptr,
-                                           nullptr);
-    DSD_CUDA(cudaGetLastError());
-    ++R.launches;
-    if (R.place_pending) place_lanes(R);
+    hbm_carveout(hgrid_of(R.place_n ? R.place_n : static_cast<int64_t>(R.n)));
     if (R.collect) {
         // size the sequence arena exactly: prefix sum of per-replica output totals
         R.host_ltot.resize(R.n);
@@ -891,7 +900,10 @@ void DeviceRuntime::launch() {
     R.smem_launch = smem;
     if (smem) {
         // AWC with staged weights: one block of awc_warps_smem warps per SM
-        const unsigned sthreads = R.awc_warps_smem > 0 ? static_cast<unsigned>(R.awc_warps_smem * kLanes) : kBlock;
+        const unsigned sthreads =
+            R.awc_warps_smem > 0
+                ? static_cast<unsigned>(awc_block_warps(R, R.awc_warps_smem, R.place_n ? R.place_n : static_cast<int64_t>(R.n)) * kLanes)
+                : kBlock;
         const size_t bytes = (R.awc_warps_smem > 0 ? R.awc_wbytes : 0) +
                              static_cast<size_t>(sthreads / kLanes) * smem_warp_bytes(R.W.c.ns, R.smem_heap, R.W.c.awc != 0);
         const int32_t* pcount = R.place_n ? static_cast<const int32_t*>(R.place.p) : nullptr;
@@ -993,7 +1005,7 @@ static void retry_heap_overflows(RuntimeImpl& R) {
         W2.c.hc = hc;
         W2.h_time = static_cast<int64_t*>(R.heap2.p);
         W2.h_key = reinterpret_cast<uint64_t*>(W2.h_time + slots);
-        const HbmCfg hc_cfg = hbm_cfg(R);
+        const HbmCfg hc_cfg = hbm_cfg(R, static_cast<int64_t>(R.n));
         k_stage<<<grid, kBlock, 0, R.stream>>>(W2, nullptr, list, count);
         (R.W.c.awc ? k_simulate<false, false, false, true> : k_simulate<false, false>)<<<
             static_cast<unsigned>((R.n + hc_cfg.threads - 1) / hc_cfg.threads), hc_cfg.threads, hc_cfg.smem,
