@@ -1,7 +1,9 @@
-// glibc_math.cuh — glibc 2.39's exp() and log() restated for the device, so
-// the workload generator (proj/src/sim/rng.cpp:63-77: exponential gaps,
-// lognormal lengths) and the AWC SiLU (proj/src/awc/kernels_scalar.cpp:65-70)
-// round exactly as the reference does on its x86-64 host.
+// glibc_math.cuh — glibc 2.39's exp(), log() and cos() restated for the
+// device, so the workload generator (proj/src/sim/rng.cpp:63-77: exponential
+// gaps, Box-Muller lognormal lengths) and the AWC SiLU
+// (proj/src/awc/kernels_scalar.cpp:65-70) round exactly as the reference does
+// on its x86-64 host.  (cos: the IBM routine below; sqrt is correctly
+// rounded on both sides.)
 //
 // glibc takes both from ARM's optimized-routines (sysdeps/ieee754/dbl-64/
 // e_exp.c, e_log.c): a 128-entry table + short polynomial.  On x86-64 with
@@ -172,6 +174,97 @@ DSD_GLIBC_FN double log(double x) {
     const double p = fma_(r2, fma_(r, A[4], A[3]), fma_(r, A[2], A[1]));
     const double y = fma_(r * r2, p, fma_(r2, A[0], lo)) + hi;
     return y;
+}
+
+// ---- __cos (glibc 2.39 sysdeps/ieee754/dbl-64/s_sin.c, IBM Accurate
+// Mathematical Library, FMA variant) for |x| < 105414350: table lookup at
+// the nearest k/128 plus short Taylor corrections, pi/2 reduction in three
+// parts.  Constants: usncs.h / s_sin.c (as in libm's constant pool).
+namespace sincos_c {
+constexpr double s1 = -0x1.5555555555555p-3, s2 = 0x1.1111111110ecep-7, s3 = -0x1.a01a019db08b8p-13,
+                 s4 = 0x1.71de27b9a7ed9p-19, s5 = -0x1.addffc2fcdf59p-26;
+constexpr double sn3 = -0x1.5555555555515p-3, sn5 = 0x1.11110e829872fp-7;
+constexpr double cs2 = 0x1p-1, cs4 = -0x1.5555555555535p-5, cs6 = 0x1.6c16bedd9e239p-10;
+constexpr double big = 0x1.8p45;
+constexpr double hp0 = 0x1.921fb54442d18p0, hp1 = 0x1.1a62633145c07p-54;
+constexpr double mp1 = 0x1.921fb58000000p0, mp2 = -0x1.dde973c000000p-27;
+constexpr double pp3 = -0x1.cb3b398000000p-55, pp4 = -0x1.d747f23e32ed7p-83;
+constexpr double hpinv = 0x1.45f306dc9c883p-1, toint = 0x1.8p52;
+}  // namespace sincos_c
+
+// TAYLOR_SIN(xx, a, da): a - a^3/3! + a^5/5! - a^7/7! + a^9/9! + (1 - a^2) da / 2
+DSD_GLIBC_FN double taylor_sin(double xx, double a, double da) {
+    using namespace sincos_c;
+    // POLYNOMIAL(xx) = ((((s5 xx + s4) xx + s3) xx + s2) xx) + s1
+    const double poly = fma_(fma_(fma_(fma_(s5, xx, s4), xx, s3), xx, s2), xx, s1);
+    // t = (POLYNOMIAL * a - 0.5 * da) * xx + da
+    const double t = fma_(fma_(poly, a, -(0.5 * da)), xx, da);
+    return a + t;
+}
+
+// do_cos(x, dx): cos(x + dx) from the table entry nearest |x|
+DSD_GLIBC_FN double do_cos(double x, double dx) {
+    using namespace sincos_c;
+    if (x < 0) dx = -dx;
+    const double ux = big + fabs(x);
+    x = fabs(x) - (ux - big) + dx;
+    const double xx = x * x;
+    const double s = fma_(x * xx, fma_(xx, sn5, sn3), x);         // x + x*xx*(sn3 + xx*sn5)
+    const double c = xx * fma_(xx, fma_(xx, cs6, cs4), cs2);      // xx*(cs2 + xx*(cs4 + xx*cs6))
+    const int k = static_cast<int>(as_u64(ux) & 0xffffffffu) << 2;  // SINCOS_TABLE_LOOKUP
+    const double sn = kSinCosTab[k], ssn = kSinCosTab[k + 1], cs = kSinCosTab[k + 2], ccs = kSinCosTab[k + 3];
+    // cor = (ccs - s*ssn - cs*c) - sn*s
+    const double cor = fma_(-sn, s, fma_(-cs, c, fma_(-s, ssn, ccs)));
+    return cs + cor;
+}
+
+// do_sin(x, dx): sin(x + dx)
+DSD_GLIBC_FN double do_sin(double x, double dx) {
+    using namespace sincos_c;
+    const double xold = x;
+    if (fabs(x) < 0.126) return taylor_sin(x * x, x, dx);
+    if (x <= 0) dx = -dx;
+    const double ux = big + fabs(x);
+    x = fabs(x) - (ux - big);
+    const double xx = x * x;
+    const double s = x + fma_(x * xx, fma_(xx, sn5, sn3), dx);   // x + (dx + x*xx*(sn3 + xx*sn5))
+    const double c = fma_(x, dx, xx * fma_(xx, fma_(xx, cs6, cs4), cs2));  // x*dx + xx*(cs2 + ...)
+    const int k = static_cast<int>(as_u64(ux) & 0xffffffffu) << 2;
+    const double sn = kSinCosTab[k], ssn = kSinCosTab[k + 1], cs = kSinCosTab[k + 2], ccs = kSinCosTab[k + 3];
+    // cor = (ssn + s*ccs - sn*c) + cs*s
+    const double cor = fma_(cs, s, fma_(-sn, c, fma_(s, ccs, ssn)));
+    const double r = sn + cor;
+    return xold < 0 ? -fabs(r) : fabs(r);  // copysign(sn + cor, xold)
+}
+
+DSD_GLIBC_FN double cos(double x) {
+    using namespace sincos_c;
+    const uint32_t k = static_cast<uint32_t>(as_u64(x) >> 32) & 0x7fffffffu;
+    if (k < 0x3e400000u) return 1.0;                 // |x| < 2^-27
+    if (k < 0x3feb6000u) return do_cos(x, 0);       // |x| < 0.855469
+    if (k < 0x400368fdu) {                           // 0.855469 < |x| < 2.426265
+        const double y = hp0 - fabs(x);
+        const double a = y + hp1;
+        const double da = (y - a) + hp1;
+        return do_sin(a, da);
+    }
+    if (k < 0x419921fbu) {                           // 2.426265 < |x| < 105414350: reduce_sincos
+        const double t = fma_(x, hpinv, toint);
+        const double xn = t - toint;
+        const double y = fma_(-xn, mp2, fma_(-xn, mp1, x));  // (x - xn*mp1) - xn*mp2
+        const int n = static_cast<int>(as_u64(t) & 3u);
+        double t1 = xn * pp3;
+        const double t2 = y - t1;
+        double db = (y - t2) - t1;
+        t1 = xn * pp4;
+        const double b = t2 - t1;
+        db += (t2 - b) - t1;
+        // do_sincos(b, db, n + 1)
+        const int m = n + 1;
+        const double r = (m & 1) ? do_cos(b, db) : do_sin(b, db);
+        return (m & 2) ? -r : r;
+    }
+    return x - x;  // (|x| >= 105414350: outside the generator's domain; not restated)
 }
 
 }  // namespace glibc

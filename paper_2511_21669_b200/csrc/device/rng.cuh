@@ -17,14 +17,16 @@
 
 #include "glibc_math.cuh"
 
-// exp / log as the reference's x86-64 glibc computes them: glibc's own
-// algorithms on the device (glibc_math.cuh), the host's libm on the host
+// exp / log / cos as the reference's x86-64 glibc computes them: glibc's
+// own algorithms on the device (glibc_math.cuh), the host's libm on the host
 #ifdef __CUDA_ARCH__
 #define DSD_EXP(x) ::dsd::glibc::exp(x)
 #define DSD_LOG(x) ::dsd::glibc::log(x)
+#define DSD_COS(x) ::dsd::glibc::cos(x)
 #else
 #define DSD_EXP(x) std::exp(x)
 #define DSD_LOG(x) std::log(x)
+#define DSD_COS(x) std::cos(x)
 #endif
 
 namespace dsd {
@@ -103,7 +105,7 @@ struct Rng {
     DSD_HD double normal(double mean, double stddev) {
         double u1 = 1.0 - unit();
         double u2 = unit();
-        double z = sqrt(-2.0 * DSD_LOG(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+        double z = sqrt(-2.0 * DSD_LOG(u1)) * DSD_COS(2.0 * 3.14159265358979323846 * u2);
         return mean + stddev * z;
     }
     DSD_HD double lognormal(double mu, double sigma) { return DSD_EXP(normal(mu, sigma)); }

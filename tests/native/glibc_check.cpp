@@ -1,7 +1,7 @@
 // glibc_check.cpp — TEST INFRASTRUCTURE: the product's restatement of glibc's
 // exp / log (paper_2511_21669_b200/csrc/device/glibc_math.cuh, host build)
 // against the host's libm, bit for bit, on the generator's argument domains
-// and well beyond.  Prints "<inputs> <log mismatches> <exp mismatches>".
+// and well beyond.  Prints "<inputs> <log mismatches> <exp mismatches> <cos mismatches>".
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -14,7 +14,7 @@
 int main(int argc, char** argv) {
     const long n = argc > 1 ? std::atol(argv[1]) : 10000000;
     std::mt19937_64 g(20251019);
-    long mm_l = 0, mm_e = 0;
+    long mm_l = 0, mm_e = 0, mm_c = 0;
     for (long t = 0; t < n; ++t) {
         const double u = static_cast<double>(g() >> 11) * 0x1.0p-53;
         // log: 1 - u (exponential gaps, Box-Muller radius) and positive doubles of all scales
@@ -32,7 +32,15 @@ int main(int argc, char** argv) {
             if (mm_e < 5) std::printf("exp %a: glibc %a restated %a\n", xe, a, b);
             ++mm_e;
         }
+        // cos: the Box-Muller angle 2*pi*u, and [-100, 100]
+        const double xc = t % 2 ? 2.0 * 3.14159265358979323846 * u : (u - 0.5) * 200.0;
+        a = std::cos(xc);
+        b = dsd::glibc::cos(xc);
+        if (std::memcmp(&a, &b, 8)) {
+            if (mm_c < 5) std::printf("cos %a: glibc %a restated %a\n", xc, a, b);
+            ++mm_c;
+        }
     }
-    std::printf("%ld %ld %ld\n", n, mm_l, mm_e);
+    std::printf("%ld %ld %ld %ld\n", n, mm_l, mm_e, mm_c);
     return 0;
 }

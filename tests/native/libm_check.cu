@@ -3,9 +3,9 @@
 // (proj/src/sim/rng.cpp:63-77, trace.cpp:145-187), which the product's
 // k_stage evaluates on the device (paper_2511_21669_b200/csrc/device/rng.cuh).
 // Compiled with the product's floating-point flags (-fmad=false,
-// -ffp-contract=off).  log and exp are evaluated with the product's
-// restatement of glibc's algorithms (glibc_math.cuh, what k_stage and the AWC
-// SiLU call); cos with CUDA libm (what k_stage still calls).  Inputs come from xoshiro256** streams seeded like the
+// -ffp-contract=off).  All three are evaluated with the product's
+// restatement of glibc's algorithms (glibc_math.cuh), what k_stage and the
+// AWC SiLU call.  Inputs come from xoshiro256** streams seeded like the
 // generator's; each function is checked on its real argument set:
 //   fn 0  log(1 - u)                 exponential gaps and Box-Muller radius
 //   fn 1  cos(2 * pi * u)            Box-Muller angle
@@ -55,7 +55,7 @@ __global__ void k_eval(int fn, const double* x, double* y, int64_t n) {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const double v = x[i];
-        y[i] = fn == 0 ? dsd::glibc::log(v) : fn == 1 ? cos(v) : dsd::glibc::exp(v);
+        y[i] = fn == 0 ? dsd::glibc::log(v) : fn == 1 ? dsd::glibc::cos(v) : dsd::glibc::exp(v);
     }
 }
 

@@ -2,8 +2,8 @@
 weak 1b).  k_stage evaluates the generator's log / cos / exp with CUDA libm
 while the reference uses glibc (proj/src/sim/rng.cpp:63-77): a 1-ulp
 difference changes an integer only at an exact .5 boundary of llround (a
-length, an arrival microsecond).  log and exp now run glibc's own algorithms
-on the device (glibc_math.cuh) and must match bit for bit; cos is CUDA's.
+length, an arrival microsecond).  All three now run glibc's own algorithms
+on the device (glibc_math.cuh) and must match bit for bit.
 This checks >= 1e8 inputs per function from the generator's real argument
 domains (tests/native/libm_check.cu) and reports the bitwise mismatches and
 the integer flips they would cause."""
@@ -27,9 +27,6 @@ def test_device_libm_matches_glibc(fn, name):
                         ctypes.byref(ex)) == 0
     print(json.dumps({"function": name, "inputs": N, "bitwise_mismatches": mm.value, "integer_flips": flips.value,
                       "example_input": ex.value if mm.value else None}))
-    # log / exp: glibc's own algorithms on the device (glibc_math.cuh) - bit
-    # for bit; cos is still CUDA's: what the engine consumes is the rounded
-    # integers, which must not move
-    if fn in (0, 2):
-        assert mm.value == 0, f"{name}: {mm.value} of {N} differ from glibc"
+    # glibc's own algorithms on the device (glibc_math.cuh): bit for bit
+    assert mm.value == 0, f"{name}: {mm.value} of {N} differ from glibc ({flips.value} change an integer)"
     assert flips.value == 0, f"{name}: {flips.value} of {N} inputs change an integer ({mm.value} differ bitwise)"
