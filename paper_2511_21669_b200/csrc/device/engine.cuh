@@ -495,6 +495,7 @@ struct Engine {
     uint64_t* hkb;   // heap keys  [hcap]
     int32_t hcap;
     int32_t nsc;
+    int32_t lst;  // lane stride of sb / htb / hkb (lstride())
     // hot scenario parameters: packed policy flags + the static window
     // fused_everything | pair_stats<<1 | lab<<2 | jitter_free<<3 | window<<4 | routing<<6 |
     // has_order<<8 | single_link<<9 | batching_window<<10
@@ -520,11 +521,11 @@ struct Engine {
     DSD_HD Engine(const Workspace& w, const DevScenario& s, int64_t replica, int32_t* server_base,
                   int64_t* heap_time_base, uint64_t* heap_key_base, int64_t heap_cap, int32_t server_cap,
                   unsigned char* hot_base = nullptr, bool specialized = false, AwcWarpScratch* awc_scratch = nullptr,
-                  int spec_stack_limit = kSpecStack)
+                  int spec_stack_limit = kSpecStack, int32_t lane_stride = kLanes, ReqRec* records = nullptr)
         : W(w), S(s), rep(static_cast<int32_t>(replica)), sb(server_base), htb(heap_time_base),
-          hkb(heap_key_base), hcap(static_cast<int32_t>(heap_cap)), nsc(server_cap), spec(specialized),
-          spec_limit(spec_stack_limit) {
-        R = W.req + replica * W.c.nr;
+          hkb(heap_key_base), hcap(static_cast<int32_t>(heap_cap)), nsc(server_cap), lst(lane_stride),
+          spec(specialized), spec_limit(spec_stack_limit) {
+        R = records ? records : W.req + replica * W.c.nr;
         gamma_s = S.gamma;
         max_batch = S.max_batch;
         dmax_batch = S.draft_max_batch;
@@ -601,7 +602,10 @@ struct Engine {
     };
 #define SV(field, i) sv(F_##field, (i))
     // (32-bit index math: server and heap blocks are far below 2^31 elements)
-    DSD_HD int32_t& sv(int f, int32_t v) const { return sb[(f * nsc + v) * kLanes]; }
+    // lane stride of the per-warp state blocks: kLanes when a warp's lanes
+    // interleave their replicas, 1 in solo mode (one replica per block)
+    DSD_HD int32_t lstride() const { return spec ? kLanes : lst; }
+    DSD_HD int32_t& sv(int f, int32_t v) const { return sb[(f * nsc + v) * lstride()]; }
     // Server::busy_us (engine.cpp:562) as two 32-bit halves in the server block
     DSD_HD int64_t get_busy(int32_t v) const {
         return static_cast<int64_t>((static_cast<uint64_t>(static_cast<uint32_t>(SV(v_busy_hi, v))) << 32) |
@@ -615,8 +619,8 @@ struct Engine {
     DSD_HD bool armed(int32_t v) const { return SV(v_flags, v) & 2; }
     DSD_HD void set_busy_flag(int32_t v, bool b) { SV(v_flags, v) = (SV(v_flags, v) & ~1) | (b ? 1 : 0); }
     DSD_HD void set_armed(int32_t v, bool b) { SV(v_flags, v) = (SV(v_flags, v) & ~2) | (b ? 2 : 0); }
-    DSD_HD int64_t& ht(int32_t k) const { return htb[k * kLanes]; }
-    DSD_HD uint64_t& hk(int32_t k) const { return hkb[k * kLanes]; }
+    DSD_HD int64_t& ht(int32_t k) const { return htb[k * lstride()]; }
+    DSD_HD uint64_t& hk(int32_t k) const { return hkb[k * lstride()]; }
 
     // ---- action stack ----
     static DSD_HD uint32_t act(uint32_t kind, uint32_t arg) { return kind | (arg << 4); }

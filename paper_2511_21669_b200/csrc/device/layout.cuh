@@ -222,6 +222,10 @@ struct Workspace {
     // ... and per replica [n][3]: vote rounds it ran in, session-loop
     // iterations (builds with -DDSD_REP_STATS), cycles from init to finish
     unsigned long long* rep_stats;
+    // solo mode (small batches of large topologies): one replica per block of
+    // one warp, lane 0; its server state and an event heap of solo_hcap slots
+    // in shared memory at lane stride 1, and (solo_rec) its request records too
+    int32_t solo, solo_hcap, solo_rec, pad_solo;
     // AWC batches: blob offset / double count of the one WC-DNN (transposed
     // layout) the kAwc blocks stage into shared memory, or -1
     int64_t awc_stage_off;

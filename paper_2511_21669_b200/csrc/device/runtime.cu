@@ -137,8 +137,13 @@ __global__ void __launch_bounds__(kAwc ? kAwcMaxThreads : kBlock,
                                   kAwc ? 1 : (kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_BLOCKS))
     k_simulate(const __grid_constant__ Workspace W, const int32_t* list, const int32_t* count, int32_t smem_heap_cap) {
     int64_t rep = 0;
-    const bool live = replica_of(W, list, count, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x, rep);
+    // solo mode: replica = block, run by lane 0 (the other lanes help copy)
+    const bool solo = kSmem && !kSpec && W.solo;
+    const bool live = solo ? (threadIdx.x == 0 && replica_of(W, list, count, blockIdx.x, rep))
+                           : replica_of(W, list, count, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x, rep);
     const int64_t r = live ? rep : 0;
+    int32_t lstride = kLanes;
+    ReqRec* srec = nullptr;
     int32_t* sbase;
     int64_t* hb;
     uint64_t* kb;
@@ -161,7 +166,34 @@ __global__ void __launch_bounds__(kAwc ? kAwcMaxThreads : kBlock,
             smem = smem_all + ((static_cast<int64_t>(W.awc_stage_n) * 8 + 127) & ~int64_t(127));
         }
     }
-    if constexpr (kSmem) {
+    if (solo) {
+        // [AWC scratch][servers 8 x ns int32][heap times][heap keys][records]
+        unsigned char* blk = smem;
+        if constexpr (kAwc) {
+            awc = reinterpret_cast<AwcWarpScratch*>(blk);
+            blk += (sizeof(AwcWarpScratch) + 15) & ~size_t(15);
+        }
+        nsc = static_cast<int32_t>(W.c.ns);
+        hcap = W.solo_hcap;
+        lstride = 1;
+        sbase = reinterpret_cast<int32_t*>(blk);
+        blk += (static_cast<int64_t>(kServerFields) * nsc * 4 + 15) & ~int64_t(15);
+        hb = reinterpret_cast<int64_t*>(blk);
+        kb = reinterpret_cast<uint64_t*>(blk + hcap * 8);
+        blk += hcap * 16;
+        int64_t sr = 0;  // the block's replica (every lane copies its records)
+        const bool has = replica_of(W, list, count, blockIdx.x, sr);
+        if (W.solo_rec && has) {
+            srec = reinterpret_cast<ReqRec*>(blk);
+            const DevScenario& S0 = W.scen[W.rep_scen[sr]];
+            const int64_t nreq = S0.workload == 0 ? S0.n_requests : S0.tr_n;
+            const uint4* src = reinterpret_cast<const uint4*>(W.req + sr * W.c.nr);
+            uint4* dst = reinterpret_cast<uint4*>(srec);
+            for (int64_t k = threadIdx.x; k < nreq * static_cast<int64_t>(sizeof(ReqRec) / 16); k += blockDim.x)
+                dst[k] = src[k];
+        }
+        __syncwarp();
+    } else if constexpr (kSmem) {
         const int lane = threadIdx.x % kLanes;
         nsc = kSpec ? 2 : static_cast<int32_t>(W.c.ns);
         hcap = smem_heap_cap;
@@ -184,7 +216,7 @@ __global__ void __launch_bounds__(kAwc ? kAwcMaxThreads : kBlock,
         if constexpr (kAwc) awc = reinterpret_cast<AwcWarpScratch*>(smem) + threadIdx.x / kLanes;
     }
     if constexpr (kAwc) awc->req[threadIdx.x % kLanes] = 0;
-    Engine e(W, W.scen[W.rep_scen[r]], r, sbase, hb, kb, hcap, nsc, hot, kSpec, awc, kSpecLimit);
+    Engine e(W, W.scen[W.rep_scen[r]], r, sbase, hb, kb, hcap, nsc, hot, kSpec, awc, kSpecLimit, lstride, srec);
     if (live) e.init();
     uint32_t kind = live ? e.next_kind() : static_cast<uint32_t>(kActNone);
     // kStats: per-step-kind cycle profile (DSD_STEP_STATS=1), one block-level
@@ -201,15 +233,23 @@ __global__ void __launch_bounds__(kAwc ? kAwcMaxThreads : kBlock,
         // AWC decisions requested during the last chains: the whole warp
         // evaluates each requester's network (warp-uniform branch)
         if constexpr (kAwc) awc_serve_warp(W.blob, &e.S, awc, awc_w, W.awc_stage_off);
-        // the kind most lanes have pending (majority vote)
-        const unsigned peers = __match_any_sync(0xffffffffu, kind);
-        const unsigned score = kind == kActNone ? 0u : vote_score(static_cast<unsigned>(__popc(peers)), kind);
-        const unsigned best = __reduce_max_sync(0xffffffffu, score);
-        if (best == 0u) break;
-        if constexpr (kStats) {  // warp rounds per selected kind (lanes per round = steps / rounds)
-            if ((threadIdx.x & (kLanes - 1)) == 0) atomicAdd(&W.step_stats[40 + vote_kind(best)], 1ull);
+        // the kind most lanes have pending (majority vote); a solo replica
+        // without AWC decisions runs alone (the idle lanes leave)
+        uint32_t sel;
+        if (solo && !kAwc) {
+            if (kind == kActNone) break;
+            sel = kind;
+        } else {
+            const unsigned peers = __match_any_sync(0xffffffffu, kind);
+            const unsigned score = kind == kActNone ? 0u : vote_score(static_cast<unsigned>(__popc(peers)), kind);
+            const unsigned best = __reduce_max_sync(0xffffffffu, score);
+            if (best == 0u) break;
+            sel = vote_kind(best);
         }
-        if (kind == vote_kind(best)) {
+        if constexpr (kStats) {  // warp rounds per selected kind (lanes per round = steps / rounds)
+            if ((threadIdx.x & (kLanes - 1)) == 0) atomicAdd(&W.step_stats[40 + sel], 1ull);
+        }
+        if (kind == sel) {
             if constexpr (kStats) ++my_rounds;
             // the selected lanes run their continuation chain up to the next
             // barrier kind (kBarrierKinds)
@@ -239,6 +279,18 @@ __global__ void __launch_bounds__(kAwc ? kAwcMaxThreads : kBlock,
         for (int k = threadIdx.x; k < 2 * kActKinds; k += blockDim.x) atomicAdd(&W.step_stats[k], blk_stats[k]);
     }
     if (live) e.finish();
+    if (solo && srec && W.collect) {  // the records export reads them from HBM
+        __syncwarp();
+        int64_t sr = 0;
+        if (replica_of(W, list, count, blockIdx.x, sr) && W.fail[sr] == kFailNone) {
+            const DevScenario& S0 = W.scen[W.rep_scen[sr]];
+            const int64_t nreq = S0.workload == 0 ? S0.n_requests : S0.tr_n;
+            const uint4* src = reinterpret_cast<const uint4*>(srec);
+            uint4* dst = reinterpret_cast<uint4*>(W.req + sr * W.c.nr);
+            for (int64_t k = threadIdx.x; k < nreq * static_cast<int64_t>(sizeof(ReqRec) / 16); k += blockDim.x)
+                dst[k] = src[k];
+        }
+    }
     if constexpr (kStats) {
         if (live && W.rep_stats) {
             W.rep_stats[3 * rep] = my_rounds;
@@ -380,6 +432,9 @@ struct RuntimeImpl {
     bool spec_stack_limit1 = false;  // DSD_SPEC_STACK_LIMIT=1 (tests: force the HBM re-run)
     bool session_fast = true;        // Engine::session_run in the specialised kernel (DSD_SESSION_FAST=0: off)
     bool awc_stage = true;           // stage one shared WC-DNN per block in shared memory (DSD_AWC_STAGE=0: off)
+    int solo = 1;  // solo mode (DSD_SOLO): 0 off, 1 topologies past kSmemServers, 2 any topology
+    int solo_heap = 0;     // DSD_SOLO_HEAP: cap on its heap slots (tests: force the HBM re-run)
+    bool solo_rec = true;  // DSD_SOLO_REC=0: keep the records in HBM
     bool smem_launch = false;
     void* pinned = nullptr;  // host_summaries() buffer (page-locked)
     bool pinned_valid = false;  // it holds the last launch's summaries
@@ -433,6 +488,9 @@ DeviceRuntime::DeviceRuntime(int device) : impl_(new RuntimeImpl) {
     if (const char* s = std::getenv("DSD_SPECIALIZE")) impl_->specialize = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_SESSION_FAST")) impl_->session_fast = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_AWC_STAGE")) impl_->awc_stage = std::atoi(s) != 0;
+    if (const char* s = std::getenv("DSD_SOLO")) impl_->solo = std::atoi(s);
+    if (const char* s = std::getenv("DSD_SOLO_HEAP")) impl_->solo_heap = std::max(0, std::atoi(s));
+    if (const char* s = std::getenv("DSD_SOLO_REC")) impl_->solo_rec = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_PLACEMENT")) impl_->placement = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_SPREAD")) impl_->spread = std::atoi(s) != 0;
     if (const char* s = std::getenv("DSD_SPREAD_MAX")) impl_->spread_max = std::atof(s);
@@ -799,6 +857,50 @@ static void place_lanes(RuntimeImpl& R) {
     }
 }
 
+// Solo mode: a batch of at most one wave of replicas whose server state
+// does not fit the shared-memory variant's per-lane layout (more than
+// kSmemServers servers: C2-C4) runs one replica per block of one warp, its
+// servers and an event heap in shared memory at lane stride 1 and, when
+// they fit next to the heap, the batch's staged WC-DNN weights (AWC) and all
+// its request records.  The per-warp HBM layout would leave every dependent state access
+// an L2 round trip for a lone replica.  A heap overflow hands the replica to
+// the HBM re-run like the shared-memory variant's.
+struct SoloCfg {
+    bool on = false;
+    int32_t hcap = 0;
+    bool rec = false;
+    bool stage = false;  // the block stages the batch's one WC-DNN (AWC)
+    size_t bytes = 0;
+};
+static SoloCfg solo_cfg(const RuntimeImpl& R) {
+    SoloCfg s;
+    const Caps& c = R.W.c;
+    if (R.solo == 0 || R.n == 0 || (R.solo == 1 && c.ns <= kSmemServers)) return s;
+    const int64_t per_sm = (static_cast<int64_t>(R.n) + R.sms - 1) / R.sms;
+    if (per_sm > 32) return s;  // one wave of one-warp blocks
+    const int64_t budget =
+        std::min<int64_t>(R.smem_optin, R.smem_per_sm / per_sm) - 1024;  // (static shared memory: the step stats)
+    int64_t fixed = (c.awc ? ((static_cast<int64_t>(sizeof(AwcWarpScratch)) + 15) & ~int64_t(15)) : 0) +
+                    ((static_cast<int64_t>(kServerFields) * c.ns * 4 + 15) & ~int64_t(15));
+    // heap: 1,024 slots or 2 per server (C4-static/-AWC single runs peak below
+    // 1,024; an overflow costs an HBM re-run, not a wrong result)
+    const int64_t hmin = std::min<int64_t>(R.solo_heap > 0 ? R.solo_heap : c.hc, std::max<int64_t>(1024, 2 * c.ns));
+    if (fixed + 16 * hmin > budget) return s;
+    // AWC: the staged weights when they fit too (every decision reads all of them)
+    if (R.W.awc_stage_off >= 0 && fixed + static_cast<int64_t>(R.awc_wbytes) + 16 * hmin <= budget) {
+        s.stage = true;
+        fixed += static_cast<int64_t>(R.awc_wbytes);
+    }
+    const int64_t recb = c.nr * static_cast<int64_t>(sizeof(ReqRec));
+    s.rec = R.solo_rec && fixed + recb + 16 * hmin <= budget;
+    // (records left in HBM: the heap stays at hmin, the rest of the array is L1 for them)
+    s.hcap = static_cast<int32_t>(s.rec ? std::min<int64_t>(c.hc, (budget - fixed - recb) / 16) : hmin);
+    if (R.solo_heap > 0) s.hcap = std::min(s.hcap, R.solo_heap);
+    s.bytes = static_cast<size_t>(fixed + 16 * s.hcap + (s.rec ? recb : 0));
+    s.on = true;
+    return s;
+}
+
 void DeviceRuntime::launch() {
     RuntimeImpl& R = *impl_;
     if (!R.prepared) throw Error(DSD_ERR_RUNTIME, "launch without a prepared batch");
@@ -896,9 +998,32 @@ void DeviceRuntime::launch() {
         R.W.rep_stats = R.W.step_stats + 64;
     }
     DSD_CUDA(cudaEventRecord(R.ev[1], R.stream));
-    const bool smem = R.W.c.ns <= kSmemServers && R.smem_heap > 0;
+    const SoloCfg solo = solo_cfg(R);
+    const bool smem = solo.on || (R.W.c.ns <= kSmemServers && R.smem_heap > 0);
     R.smem_launch = smem;
-    if (smem) {
+    if (solo.on) {
+        Workspace Ws = R.W;
+        Ws.solo = 1;
+        Ws.solo_hcap = solo.hcap;
+        Ws.solo_rec = solo.rec ? 1 : 0;
+        if (!solo.stage) Ws.awc_stage_off = -1;
+        auto k = R.W.c.awc ? (R.step_stats ? k_simulate<true, true, false, true> : k_simulate<true, false, false, true>)
+                           : (R.step_stats ? k_simulate<true, true> : k_simulate<true, false>);
+        cudaFuncAttributes fa;
+        DSD_CUDA(cudaFuncGetAttributes(&fa, k));
+        DSD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      R.smem_optin - static_cast<int>(fa.sharedSizeBytes)));
+        int pct = R.carveout;
+        if (pct < 0) {
+            const int64_t per_sm = (static_cast<int64_t>(R.n) + R.sms - 1) / R.sms;
+            pct = static_cast<int>(std::min<int64_t>(
+                100, (100 * per_sm * (static_cast<int64_t>(solo.bytes) + 1024) + R.smem_per_sm - 1) / R.smem_per_sm));
+        }
+        DSD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+        k<<<static_cast<unsigned>(R.n), kLanes, solo.bytes, R.stream>>>(Ws, nullptr, nullptr, 0);
+        DSD_CUDA(cudaGetLastError());
+        ++R.launches;
+    } else if (smem) {
         // AWC with staged weights: one block of awc_warps_smem warps per SM
         const unsigned sthreads =
             R.awc_warps_smem > 0
@@ -940,6 +1065,9 @@ void DeviceRuntime::launch() {
             (R.step_stats ? k_simulate<true, true> : k_simulate<true, false>)<<<sgrid, kBlock, bytes, R.stream>>>(
                 R.W, plist, pcount, R.smem_heap);
         DSD_CUDA(cudaGetLastError());
+        ++R.launches;
+    }
+    if (smem) {
         // replicas whose event heap outgrew shared memory run again from HBM
         R.ovf.ensure(4 * (R.n + 1));
         int32_t* count = static_cast<int32_t*>(R.ovf.p);
@@ -952,7 +1080,7 @@ void DeviceRuntime::launch() {
         (R.W.c.awc ? (R.step_stats ? k_simulate<false, true, false, true> : k_simulate<false, false, false, true>)
                     : (R.step_stats ? k_simulate<false, true> : k_simulate<false, false>))<<<hgrid_of(static_cast<int64_t>(R.n)), hcfg.threads, hbm_smem, R.stream>>>(R.W, list, count, 0);
         DSD_CUDA(cudaGetLastError());
-        R.launches += 4;
+        R.launches += 3;
     } else {
         // (HBM state is indexed by replica, so a lane placement is just a thread -> replica list)
         const int32_t* pcount = R.place_n ? static_cast<const int32_t*>(R.place.p) : nullptr;

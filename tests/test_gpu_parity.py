@@ -238,6 +238,42 @@ def test_specialized_kernel_matches_generic_and_reference(smem_heap):
     assert sums["11"].tobytes() == sums["01"].tobytes() == sums["10"].tobytes()
 
 
+@pytest.mark.parametrize("env", [
+    {"DSD_SOLO": "0"},  # the per-lane HBM / shared-memory variants
+    {"DSD_SOLO": "2"},  # solo mode for the small topologies too
+    {"DSD_SOLO_REC": "0"},  # solo mode with the records left in HBM
+    {"DSD_SOLO_HEAP": "6", "DSD_HOST_TIMING": "1"},  # solo heap overflow -> HBM re-run
+])
+def test_solo_mode_matches_reference(env, gen_dir, tmp_path, capfd):
+    """Batches of at most one wave of large-topology replicas run one replica
+    per block (solo mode: servers, heap and records in shared memory); the
+    single runs, a sweep summary and the per-point report files (records
+    copied back for the export) must match the reference whichever variant
+    runs them."""
+    from paper_2511_21669_b200 import Simulator
+    spec = ("base: c2_8x1_batching.yaml\nseed: 4\nrepetitions: 2\naxes:\n"
+            "  network.rtt_ms: [1, 20]\n  policies.window.kind: [static, dynamic]\n")
+    js, cs = ref.run_sweep(spec, CFG, 4, str(tmp_path / "ref"))
+    os.environ.update(env)
+    try:
+        with Simulator(0) as s:
+            for name in ("c2_8x1_batching.yaml", "c3_64x4_awc.yaml"):
+                _compare(s, _cfg(name), gen_dir)
+            _compare(s, _cfg("c1_single_pair.yaml"))
+            out = s.run_sweep(spec, base_dir=CFG, out_dir=str(tmp_path / "mine"))
+    finally:
+        for k in env:
+            del os.environ[k]
+    assert (out.summary_json, out.summary_csv) == (js, cs)
+    files = sorted(os.listdir(tmp_path / "ref"))
+    assert files == sorted(os.listdir(tmp_path / "mine"))
+    for f in files:
+        assert (tmp_path / "ref" / f).read_bytes() == (tmp_path / "mine" / f).read_bytes(), f
+    if "DSD_SOLO_HEAP" in env:
+        m = re.findall(r"re-run on the HBM variant: (\d+) of (\d+) replicas", capfd.readouterr().err)
+        assert m and max(int(a) for a, _ in m) > 0
+
+
 def test_rewritten_input_files_are_read_again(sim, tmp_path):
     """A trace and a WC-DNN model rewritten at the same path between two calls
     on one handle: the second call must use the new contents (the reference
