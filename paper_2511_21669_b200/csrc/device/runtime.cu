@@ -531,10 +531,13 @@ void DeviceRuntime::transfer_bytes(int64_t* h2d, int64_t* d2h) const {
 // of them waits through: measured on the heaviest C5 replica (gamma 1, alpha
 // 0.5) alone, a warp of 1 / 2 / 4 / 8 / 16 lanes takes 1 / 1.68 / 2.54 /
 // 3.54 / 4.57 x the time of a lone lane (kWarpSlow).  Replicas are sorted by
-// an estimate of their cost - N x (9 + median output / E[tokens per round])
+// an estimate of their cost - N x (150 + median output / E[tokens per round])
 // for a synthetic workload with a static window, E = (1 - a^(g+1)) / (1 - a):
-// about nine steps of general event handling per request plus one session
-// iteration per round - and each gets the widest warp that keeps
+// a request's general event handling (~60 steps, ~13 us on a lone lane)
+// against one session iteration (~66 ns) per round, fitted to lone-lane
+// kernel times of C5's (gamma, alpha) corners (the earlier
+// weight 9 ranked gamma-15 replicas as light and packed them 32 wide, a
+// 9 ms warp in 1/8 of C5) - and each gets the widest warp that keeps
 // cost x kWarpSlow[width] within a makespan T, the smallest T whose warps
 // all fit one wave (`warp_cap`, binary search).  So a batch that leaves room
 // (a strong-scaling shard, a small sweep) runs its heavy replicas one per
@@ -545,14 +548,19 @@ void DeviceRuntime::transfer_bytes(int64_t* h2d, int64_t* d2h) const {
 // unchanged.
 static std::vector<int32_t> placement_list(const Packed& P, size_t n, int64_t warp_cap) {
     if (n < 2) return {};
-    if (static_cast<int64_t>(n) > warp_cap * kLanes) return {};
+    // a batch that nearly fills the wave densely is issue-bound, not
+    // critical-path-bound: thin warps would only cost SIMT efficiency
+    // (C5, 65,536 replicas on 2,368 warps: dense 13.2 ms, placed 13.7 ms)
+    static const double max_fill = std::getenv("DSD_PLACE_MAX_FILL") ? std::atof(std::getenv("DSD_PLACE_MAX_FILL")) : 0.75;
+    if (static_cast<double>(n) > max_fill * static_cast<double>(warp_cap * kLanes)) return {};
     std::vector<double> est(P.scen.size(), 0.0);
+    static const double cost_req = std::getenv("DSD_COST_REQ") ? std::atof(std::getenv("DSD_COST_REQ")) : 150.0;
     for (size_t k = 0; k < P.scen.size(); ++k) {
         const DevScenario& d = P.scen[k];
         if (d.workload != 0 || d.n_drafts < 1 || d.fused_everything || d.window_kind != 0) return {};
         const double a = d.alpha, g = d.gamma;
         const double tau = a < 1.0 ? (1.0 - std::pow(a, g + 1.0)) / (1.0 - a) : g + 1.0;
-        est[k] = static_cast<double>(d.n_requests) * (9.0 + std::exp(d.o_mu) / tau);
+        est[k] = static_cast<double>(d.n_requests) * (cost_req + std::exp(d.o_mu) / tau);
     }
     // replicas by decreasing estimate: sort the scenarios, then a counting
     // sort of the replicas by their scenario's rank (replica order within one)
@@ -563,6 +571,15 @@ static std::vector<int32_t> placement_list(const Packed& P, size_t n, int64_t wa
     for (size_t i = 0; i < ns; ++i) srank[static_cast<size_t>(sorder[i])] = static_cast<int32_t>(i);
     for (size_t r = 0; r < n; ++r) ++start[static_cast<size_t>(srank[P.rep_scen[r]]) + 1];
     for (size_t i = 0; i < ns; ++i) start[i + 1] += start[i];
+    // (cost, replica count) per scenario with replicas, in cost order: the
+    // makespan search below runs over these groups, not the replicas
+    std::vector<double> gcost;
+    std::vector<int64_t> gcnt;
+    for (size_t i = 0; i < ns; ++i)
+        if (start[i + 1] > start[i]) {
+            gcost.push_back(est[static_cast<size_t>(sorder[i])]);
+            gcnt.push_back(start[i + 1] - start[i]);
+        }
     std::vector<int32_t> order(n);
     for (size_t r = 0; r < n; ++r) order[static_cast<size_t>(start[static_cast<size_t>(srank[P.rep_scen[r]])]++)] = static_cast<int32_t>(r);
     std::vector<double> cost(n);
@@ -581,15 +598,15 @@ static std::vector<int32_t> placement_list(const Packed& P, size_t n, int64_t wa
     auto warps = [&](double T) {
         int64_t total = 0, run = 0;
         int cur = -2;
-        for (size_t i = 0; i < n; ++i) {
-            const int w = width(cost[i], T);
+        for (size_t g = 0; g < gcost.size(); ++g) {
+            const int w = width(gcost[g], T);
             if (w < 0) return INT64_MAX;
             if (w != cur) {
                 if (cur >= 0) total += (run + kWidth[cur] - 1) / kWidth[cur];
                 cur = w;
                 run = 0;
             }
-            ++run;
+            run += gcnt[g];
         }
         return total + (run + kWidth[cur] - 1) / kWidth[cur];
     };
@@ -905,6 +922,15 @@ void DeviceRuntime::launch() {
     RuntimeImpl& R = *impl_;
     if (!R.prepared) throw Error(DSD_ERR_RUNTIME, "launch without a prepared batch");
     DSD_CUDA(cudaSetDevice(R.device));
+    static const bool timing = std::getenv("DSD_HOST_TIMING") != nullptr;
+    auto t_prev = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!timing) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[dsd launch] %-10s %8.2f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t - t_prev).count());
+        t_prev = t;
+    };
     R.launches = 0;
     R.rec_cached = false;
     R.pinned_valid = false;
@@ -928,7 +954,9 @@ void DeviceRuntime::launch() {
                                            nullptr);
     DSD_CUDA(cudaGetLastError());
     ++R.launches;
+    lap("stage");
     if (R.place_pending) place_lanes(R);
+    lap("placement");
     // the HBM variant's only shared memory: the cooperative AWC scratch (and
     // the staged AWC weights); its carveout keeps just that (the rest of the
     // array is L1, which holds the replicas' state)
@@ -997,6 +1025,7 @@ void DeviceRuntime::launch() {
         R.W.step_stats = static_cast<unsigned long long*>(R.stats.p);
         R.W.rep_stats = R.W.step_stats + 64;
     }
+    lap("arena");
     DSD_CUDA(cudaEventRecord(R.ev[1], R.stream));
     const SoloCfg solo = solo_cfg(R);
     const bool smem = solo.on || (R.W.c.ns <= kSmemServers && R.smem_heap > 0);
@@ -1093,6 +1122,7 @@ void DeviceRuntime::launch() {
         ++R.launches;
     }
     DSD_CUDA(cudaEventRecord(R.ev[2], R.stream));
+    lap("simulate");
     R.ran = true;
 }
 

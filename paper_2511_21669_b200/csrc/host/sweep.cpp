@@ -345,6 +345,7 @@ void launch_batch(Runtime& rt, SweepBatch& b, bool reports) {
     rt.prepare(b.scenarios.data(), b.scenarios.size(), b.replicas.data(), b.replicas.size(), reports);
     tm.lap("prepare");
     rt.launch();
+    tm.lap("launch");
 }
 
 void collect_batch(Runtime& rt, SweepBatch& b, const std::string& out_dir, SweepTotals& tot) {
@@ -442,7 +443,11 @@ SweepTotals run_sweep(Runtime& rt, SweepBatch& b, const std::string& out_dir, Su
     launch_batch(rt, b, reports);
     // the host is idle while the kernels run: render the summary text that
     // does not depend on the results
-    if (parts) *parts = render_summary_prefixes(b.points, b.point_base);
+    {
+        PhaseTimer tm("run_sweep");
+        if (parts) *parts = render_summary_prefixes(b.points, b.point_base);
+        tm.lap("prefixes");
+    }
     collect_batch(rt, b, out_dir, tot);
     return tot;
 }

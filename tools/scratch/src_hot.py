@@ -13,7 +13,8 @@ for r in rows:
         hdr = r
     elif r and r[0].isdigit() and hdr:
         d = dict(zip(hdr, r))
-        lines.append((int(d["# Samples"] or 0), int(d["Instructions Executed"] or 0), cur, r[0], r[1][:90]))
+        num = lambda x: int(x) if x.strip().lstrip("-").isdigit() else 0
+        lines.append((num(d["# Samples"]), num(d["Instructions Executed"]), cur, r[0], r[1][:90]))
 ts = sum(x[0] for x in lines)
 ti = sum(x[1] for x in lines)
 print("samples", ts, "instructions", ti)
