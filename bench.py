@@ -246,15 +246,18 @@ def main_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def roofline(ev_local, sim_ms, clk):
+def roofline(ev_local, sim_ms, clk, same_launch=True):
+    """same_launch: the committed capture is of this launch (the N=1 default
+    workload); a strong-scaling shard is a different launch, so its line
+    carries no capture-derived fields."""
     peak, peak_kind = peaks()
     achieved = B_EV * ev_local / (sim_ms / 1e3) / 1e9
-    nc = ncu_summary()
+    nc = ncu_summary() if same_launch else {}
     out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
            "traffic": nc.get("dram_bytes_per_launch"), "peak_source": peak_kind, "bytes_per_event": B_EV,
            "kernel": "k_simulate", "kernel_ms": sim_ms,
            "from_committed_capture": ["traffic", "issue.warp_instructions", "issue.threads_per_instruction",
-                                      "ncu_issue_active_pct", "ncu_stall_pct"]}
+                                      "ncu_issue_active_pct", "ncu_stall_pct"] if nc else []}
     # The DES is latency/issue-bound, not HBM-bound (DESIGN.md §3.3): the issue
     # roofline = warp instructions of the launch (deterministic for the
     # workload; from the committed capture) / (SMs x 4 schedulers x clock x
@@ -320,6 +323,7 @@ def main_ours(args, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
+        os.environ["NCCL_DEBUG"] = "WARN"  # (VERSION would print a banner on stdout before the JSON line)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     sim = Simulator(local_rank)
     _, spec, base, desc = workload_text(args.workload, world if args.weak else 1)
@@ -379,7 +383,14 @@ def main_ours(args, rank, world, local_rank):
     clk = clocks.stop() if clocks else None
 
     tot_ms = sum(step_ms)
+    per_rank = None
     if dist:
+        # every rank's step and simulate-kernel times (the max is the value)
+        mine = torch.tensor([tot_ms / args.steps, sum(sim_ms) / len(sim_ms)], dtype=torch.float64, device="cuda")
+        allr = torch.zeros(world * 2, dtype=torch.float64, device="cuda")
+        dist.all_gather_into_tensor(allr, mine)
+        per_rank = [{"ms_per_step": round(float(allr[2 * r]), 3), "sim_kernel_ms": round(float(allr[2 * r + 1]), 3)}
+                    for r in range(world)]
         t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
@@ -436,12 +447,13 @@ def main_ours(args, rank, world, local_rank):
         "replicas_per_sec": rep_all / (ms_per_step / 1e3),
         "e2e": {"value": e2e_events / e2e_s, "unit": "events/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * e2e_s, "path": e2e_path},
-        "roofline": roofline(ev_local, sim_avg, clk),
+        "roofline": roofline(ev_local, sim_avg, clk, same_launch=world == 1 and args.workload == "c5"),
         "gpu_launches": launches,
         "wall_s": wall,
     }
     if world > 1:
         line["rank0"] = {"replicas": n_rep, "events": int(ev_local), "sim_kernel_ms": sim_avg}
+        line["ranks"] = per_rank
     if clk:
         line["clocks"] = clk
     if world == 1 and not args.no_cpu_baseline:
