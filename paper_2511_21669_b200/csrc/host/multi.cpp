@@ -40,27 +40,25 @@ double replica_cost_estimate(const dsd_scenario& s) {
 std::vector<int32_t> shard_of_replicas(const dsd_scenario* sc, const dsd_replica* reps, size_t n, int n_shards) {
     std::vector<int32_t> shard(n, 0);
     if (n_shards <= 1 || n == 0) return shard;
-    // cost per distinct scenario, then replicas by decreasing cost
-    std::vector<double> cost(n);
-    {
-        std::vector<double> sc_cost;
-        std::vector<char> have;
-        for (size_t k = 0; k < n; ++k) {
-            const uint32_t s = reps[k].scenario;
-            if (s >= sc_cost.size()) {
-                sc_cost.resize(s + 1, 0.0);
-                have.resize(s + 1, 0);
-            }
-            if (!have[s]) {
-                sc_cost[s] = replica_cost_estimate(sc[s]);
-                have[s] = 1;
-            }
-            cost[k] = sc_cost[s];
-        }
-    }
+    // cost per distinct scenario; replicas by decreasing cost = the
+    // scenarios sorted by cost, then a counting sort of the replicas by their
+    // scenario's rank (replica order within a rank)
+    uint32_t ns = 0;
+    for (size_t k = 0; k < n; ++k) ns = std::max(ns, reps[k].scenario + 1);
+    std::vector<double> sc_cost(ns, 0.0);
+    std::vector<char> used(ns, 0);
+    for (size_t k = 0; k < n; ++k) used[reps[k].scenario] = 1;
+    for (uint32_t s = 0; s < ns; ++s)
+        if (used[s]) sc_cost[s] = replica_cost_estimate(sc[s]);
+    std::vector<uint32_t> sorder(ns), srank(ns);
+    std::iota(sorder.begin(), sorder.end(), 0u);
+    std::stable_sort(sorder.begin(), sorder.end(), [&](uint32_t a, uint32_t b) { return sc_cost[a] > sc_cost[b]; });
+    for (uint32_t i = 0; i < ns; ++i) srank[sorder[i]] = i;
+    std::vector<size_t> start(static_cast<size_t>(ns) + 1, 0);
+    for (size_t k = 0; k < n; ++k) ++start[srank[reps[k].scenario] + 1];
+    for (uint32_t i = 0; i < ns; ++i) start[i + 1] += start[i];
     std::vector<uint32_t> order(n);
-    std::iota(order.begin(), order.end(), 0u);
-    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cost[a] > cost[b]; });
+    for (size_t k = 0; k < n; ++k) order[start[srank[reps[k].scenario]]++] = static_cast<uint32_t>(k);
     const size_t N = static_cast<size_t>(n_shards);
     for (size_t i = 0; i < n; ++i) {
         const size_t round = i / N, pos = i % N;
