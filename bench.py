@@ -22,7 +22,7 @@ multi-device handle makes); --weak gives every GPU its own 65,536 replicas.
          (dsd_create_devices) while the other ranks wait.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--weak] [--workload c5|c2_seeds|c3_seeds|c4s_seeds|c4a_seeds|
+                  [--weak] [--workload c5|c2_seeds|c2_seeds_16k|c3_seeds|c3_seeds_4k|c4s_seeds|c4a_seeds|
                    c1_single|c2_single|c3_single|c4s_single|c4a_single]
 """
 import argparse
@@ -58,6 +58,10 @@ WORKLOADS = {
            "C1 single edge-cloud pair (BASELINE configs[4])"),
     "c2_seeds": ("sweep", _seed_sweep(os.path.join(GOLDEN, "c2_8x1_batching.yaml"), 32, 32),
                  GOLDEN, "C2 (8 drafts x 1 target, 2 ms batching window, jsq): rtt 2..33 ms x 32 seeds = 1024 replicas"),
+    "c2_seeds_16k": ("sweep", _seed_sweep(os.path.join(GOLDEN, "c2_8x1_batching.yaml"), 32, 512), GOLDEN,
+                     "C2 (8 drafts x 1 target, 2 ms batching window, jsq): rtt 2..513 ms x 32 seeds = 16384 replicas"),
+    "c3_seeds_4k": ("sweep", _seed_sweep(os.path.join(GOLDEN, "c3_64x4_awc.yaml"), 16, 256), GEN,
+                    "C3 (64 drafts x 4 targets, heterogeneous RTT, AWC) x 4096 seeds"),
     "c3_seeds": ("sweep", _seed_sweep(os.path.join(GOLDEN, "c3_64x4_awc.yaml"), 16, 16), GEN,
                  "C3 (64 drafts x 4 targets, heterogeneous RTT, AWC) x 256 seeds"),
     "c4s_seeds": ("sweep", _seed_sweep(os.path.join(GOLDEN, "c4_1024x16_static.yaml"), 4, 16), GEN,

@@ -1972,14 +1972,30 @@ DSD_HD void stage_workload(const Workspace& W, int64_t rep) {
             init_record(R[n], arr, static_cast<int32_t>(p), static_cast<int32_t>(o), dr, static_cast<int32_t>(word),
                         static_cast<int32_t>(o), static_cast<int32_t>(lsum));
             lsum += o;
-            for (int64_t k = 0; k < o; k += 64) {
-                int64_t m = o - k < 64 ? o - k : 64;
-                uint64_t acc = 0;
-                for (int j = 0; j < static_cast<int>(m); ++j) {
-                    const uint64_t b = (bitrng.next() >> 11) < accept_below ? 1u : 0u;
-                    acc |= b << j;
-                }
-                bits[word++] = acc;
+            word += (o + 63) >> 6;  // each request's bits start a word
+        }
+        // The acceptance bits (their own stream, so drawn after the records):
+        // one loop over the replica's bit words.  Per-request loops held a
+        // warp's lanes for the longest of their requests' outputs every time
+        // (half the lanes idle); here a lane waits at most for the rest of
+        // another lane's word.
+        const int64_t N = S.n_requests;
+        int32_t rem = N > 0 ? R[0].output : 0;
+        int32_t o_next = N > 1 ? R[1].output : 0;  // (loaded a request ahead)
+        int64_t nn = 1;
+        for (int64_t w = 0; w < word; ++w) {
+            const int m = rem < 64 ? rem : 64;
+            uint64_t acc = 0;
+            for (int j = 0; j < m; ++j) {
+                const uint64_t b = (bitrng.next() >> 11) < accept_below ? 1u : 0u;
+                acc |= b << j;
+            }
+            bits[w] = acc;
+            rem -= m;
+            if (rem == 0) {
+                rem = o_next;
+                ++nn;
+                o_next = nn < N ? R[nn].output : 0;
             }
         }
     } else {
