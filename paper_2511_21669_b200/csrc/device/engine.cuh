@@ -1972,16 +1972,19 @@ DSD_HD void stage_workload(const Workspace& W, int64_t rep) {
             init_record(R[n], arr, static_cast<int32_t>(p), static_cast<int32_t>(o), dr, static_cast<int32_t>(word),
                         static_cast<int32_t>(o), static_cast<int32_t>(lsum));
             lsum += o;
-            word += (o + 63) >> 6;  // each request's bits start a word
+            bits[word] = static_cast<uint64_t>(o);  // (stashed for the bit loop, which overwrites it)
+            word += (o + 63) >> 6;                   // each request's bits start a word
         }
         // The acceptance bits (their own stream, so drawn after the records):
         // one loop over the replica's bit words.  Per-request loops held a
         // warp's lanes for the longest of their requests' outputs every time
         // (half the lanes idle); here a lane waits at most for the rest of
         // another lane's word.
+        // (a request's output length comes from its stashed first word, loaded
+        // a request ahead; the records' lines are not read back)
         const int64_t N = S.n_requests;
-        int32_t rem = N > 0 ? R[0].output : 0;
-        int32_t o_next = N > 1 ? R[1].output : 0;  // (loaded a request ahead)
+        int32_t rem = N > 0 ? static_cast<int32_t>(bits[0]) : 0;
+        int32_t o_next = N > 1 ? static_cast<int32_t>(bits[(rem + 63) >> 6]) : 0;
         int64_t nn = 1;
         for (int64_t w = 0; w < word; ++w) {
             const int m = rem < 64 ? rem : 64;
@@ -1995,7 +1998,7 @@ DSD_HD void stage_workload(const Workspace& W, int64_t rep) {
             if (rem == 0) {
                 rem = o_next;
                 ++nn;
-                o_next = nn < N ? R[nn].output : 0;
+                o_next = nn < N ? static_cast<int32_t>(bits[w + 1 + ((rem + 63) >> 6)]) : 0;
             }
         }
     } else {
