@@ -244,7 +244,7 @@ def main_reference(args, rank, world):
                          "sample": last["sample"]},
         "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -314,7 +314,7 @@ def main_single(args, rank, world, local_rank):
         cb = cpu_reference(args.workload)
         line["cpu_baseline"] = {"value": cb["events"] / cb["seconds"], "unit": "events/s", "cores": cb["cores"],
                                 "kind": cb["kind"], "sample": cb["sample"]}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main_ours(args, rank, world, local_rank):
@@ -327,7 +327,6 @@ def main_ours(args, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        os.environ["NCCL_DEBUG"] = "WARN"  # (VERSION would print a banner on stdout before the JSON line)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     sim = Simulator(local_rank)
     _, spec, base, desc = workload_text(args.workload, world if args.weak else 1)
@@ -465,7 +464,7 @@ def main_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = {"value": cb["events"] / cb["seconds"], "unit": "events/s", "cores": cb["cores"],
                                 "kind": cb["kind"], "sample": cb["sample"],
                                 "replicas_per_sec": cb["replicas"] / cb["seconds"]}
-    print(json.dumps(line), flush=True)
+    emit(line)
     if dist:
         dist.destroy_process_group()
 
@@ -477,7 +476,21 @@ class _DevView:
         self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
 
 
+_STDOUT = None
+
+
+def emit(line):
+    """The one JSON line, on the process's real stdout (libraries' banners -
+    NCCL prints its version at communicator creation - go to stderr)."""
+    os.write(_STDOUT if _STDOUT is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _STDOUT
+    # everything else written to fd 1 (C libraries included) goes to stderr
+    sys.stdout.flush()
+    _STDOUT = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)

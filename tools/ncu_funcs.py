@@ -21,7 +21,7 @@ ENGINE = os.path.join(HERE, "paper_2511_21669_b200", "csrc", "device", "engine.c
 LIB = os.path.join(HERE, "paper_2511_21669_b200", "libdsdsim.so")
 
 
-def main(rep, variant="k_simulateILb1ELb0"):
+def main(rep, variant="k_simulateILb1ELb0ELb1ELb0ELi2E"):  # (the specialised production kernel)
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
