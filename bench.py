@@ -122,51 +122,80 @@ def cpu_model():
     return "unknown"
 
 
+_SAMPLER = r"""
+import sys, time
+import pynvml as nv
+nv.nvmlInit()
+hs = [nv.nvmlDeviceGetHandleByIndex(int(i)) for i in sys.argv[1].split(",")]
+masks = [(n, getattr(nv, a)) for n, a in (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+         ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+         ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+         ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))]
+smax = max(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM) for h in hs)
+print("ready", smax, flush=True)
+while True:
+    for h in hs:
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        print(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), *[n for n, m in masks if r & m], flush=True)
+    time.sleep(0.002)
+"""
+
+
 class Clocks:
-    """SM clocks and throttle reasons sampled DURING the timed region: an NVML
-    thread polling every 2 ms (the timed region of a default run is ~0.1 s,
-    too short for nvidia-smi -lms); the device's CUDA ordinals map to NVML
-    indices through CUDA_VISIBLE_DEVICES when it is set."""
-    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
-               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
-               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
-               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+    """SM clocks and throttle reasons sampled DURING the timed region by an NVML
+    poller every 2 ms in a separate process (the timed region of a default run
+    is ~0.1 s, too short for nvidia-smi -lms; a thread would contend for the
+    GIL with the launching thread).  CUDA ordinals map to NVML indices through
+    CUDA_VISIBLE_DEVICES when it is set."""
 
     def __init__(self, devices):
-        import threading
-        self.sm, self.smax, self.reasons = [], 0.0, set()
-        self.stop_ev = threading.Event()
-        self.thread = None
+        import subprocess
+        import tempfile
+        self.proc = None
         try:
-            import pynvml as nv
-            nv.nvmlInit()
             vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-            idx = [int(vis.split(",")[d]) if vis else d for d in devices]
-            self.handles = [nv.nvmlDeviceGetHandleByIndex(i) for i in idx]
-            self.smax = max(float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)) for h in self.handles)
-            masks = [(n, getattr(nv, a)) for n, a in self.REASONS]
-
-            def run():
-                while not self.stop_ev.is_set():
-                    for h in self.handles:
-                        self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
-                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                        self.reasons.update(n for n, m in masks if r & m)
-                    self.stop_ev.wait(0.002)
-            self.thread = threading.Thread(target=run, daemon=True)
-            self.thread.start()
+            idx = [vis.split(",")[d] if vis else str(d) for d in devices]
+            fd, self.path = tempfile.mkstemp(suffix=".clocks")
+            os.close(fd)
+            with open(self.path, "ab") as sink:  # O_APPEND: the reader's offset is its own
+                self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, ",".join(idx)], stdout=sink,
+                                             stderr=subprocess.DEVNULL)
+            self.smax, self.start = 0.0, None
+            t = time.time()
+            while time.time() - t < 20 and self.proc.poll() is None:  # until it samples
+                with open(self.path) as f:
+                    first = f.readline()
+                    if first.startswith("ready") and first.endswith("\n"):
+                        self.smax = float(first.split()[1])
+                        f.seek(0, 2)
+                        self.start = f.tell()  # the timed region starts after this
+                        break
+                time.sleep(0.01)
+            if self.start is None:
+                self.proc.kill()
+                self.proc = None
         except Exception:
-            self.thread = None
+            self.proc = None
 
     def stop(self):
-        if not self.thread:
+        if not self.proc:
             return None
-        self.stop_ev.set()
-        self.thread.join(timeout=5)
-        if not self.sm:
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        sm, reasons = [], set()
+        with open(self.path) as f:
+            f.seek(self.start)
+            for line in f.read().splitlines():
+                parts = line.split()
+                if not parts or parts[0] == "ready":
+                    continue
+                sm.append(float(parts[0]))
+                reasons.update(parts[1:])
+        os.unlink(self.path)
+        if not sm:
             return None
-        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.smax, "reasons": sorted(self.reasons),
-                "samples": len(self.sm), "sampler": "nvml, 2 ms"}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.smax, "reasons": sorted(reasons),
+                "samples": len(sm), "sampler": "nvml, 2 ms, own process"}
 
 
 # ---------------------------------------------------------------------------
