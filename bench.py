@@ -391,10 +391,12 @@ def main_ours(args, rank, world, local_rank):
         raise SystemExit("engine reported failed replicas")
     ev_local = float(sm["events_processed"].sum())
 
+    # (the sampler starts before the barrier: the other ranks would otherwise
+    # wait for rank 0 inside their first timed step)
+    clocks = Clocks([local_rank]) if rank == 0 else None
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = Clocks([local_rank]) if rank == 0 else None
     t0 = time.perf_counter()
     step_ms, sim_ms = [], []
     for _ in range(args.steps):
