@@ -20,6 +20,7 @@ struct Error : std::runtime_error {
 };
 
 struct RuntimeImpl;
+struct DevicePool;  // host threads of a multi-device Runtime (multi.cpp)
 
 // One GPU: packs a batch into its scenario blob + workspace and runs the
 // staging and simulation kernels on its own stream (runtime.cu).
@@ -99,7 +100,10 @@ public:
     std::vector<size_t> shard_sizes() const;
 
 private:
+    template <class F>
+    void each_device(F&& fn);
     std::vector<std::unique_ptr<DeviceRuntime>> devs_;
+    std::unique_ptr<DevicePool> pool_;  // host threads of devices 1.. (none for one device)
     // prepared batch: replica -> (device, index on it); per device its replicas' global indices
     std::vector<int32_t> dev_of_;
     std::vector<uint32_t> local_of_;

@@ -9,7 +9,9 @@
 // into page-locked memory, since one process owns every device here.
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <exception>
+#include <functional>
 #include <mutex>
 #include <numeric>
 #include <thread>
@@ -59,13 +61,86 @@ std::vector<int32_t> shard_of_replicas(const dsd_scenario* sc, const dsd_replica
     for (uint32_t i = 0; i < ns; ++i) start[i + 1] += start[i];
     std::vector<uint32_t> order(n);
     for (size_t k = 0; k < n; ++k) order[start[srank[reps[k].scenario]]++] = static_cast<uint32_t>(k);
-    const size_t N = static_cast<size_t>(n_shards);
+    // dealt 0..N-1, N-1..0, 0..N-1, ... (counters: no 64-bit division per replica)
+    int32_t pos = 0, dir = 1;
     for (size_t i = 0; i < n; ++i) {
-        const size_t round = i / N, pos = i % N;
-        shard[order[i]] = static_cast<int32_t>(round % 2 == 0 ? pos : N - 1 - pos);
+        shard[order[i]] = pos;
+        pos += dir;
+        if (pos == n_shards || pos < 0) {
+            dir = -dir;
+            pos += dir;
+        }
     }
     return shard;
 }
+
+// One persistent host thread per extra device (device 0 runs on the caller):
+// a thread that makes its first CUDA call attaches to the device's context,
+// which cost ~0.3 ms per device and call when every call spawned threads.
+// run(fn) calls fn(k) for every device concurrently and rethrows the first
+// exception once all have finished.
+struct DevicePool {
+    explicit DevicePool(size_t n) : n_(n) {
+        for (size_t k = 1; k < n; ++k)
+            th_.emplace_back([this, k] {
+                uint64_t seen = 0;
+                for (;;) {
+                    const std::function<void(size_t)>* task;
+                    {
+                        std::unique_lock<std::mutex> lk(m_);
+                        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                        if (stop_) return;
+                        seen = gen_;
+                        task = task_;
+                    }
+                    call(*task, k);
+                    std::lock_guard<std::mutex> lk(m_);
+                    if (++done_ == n_ - 1) done_cv_.notify_all();
+                }
+            });
+    }
+    ~DevicePool() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void run(const std::function<void(size_t)>& fn) {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            task_ = &fn;
+            done_ = 0;
+            first_ = nullptr;
+            ++gen_;
+        }
+        cv_.notify_all();
+        call(fn, 0);
+        std::unique_lock<std::mutex> lk(m_);
+        done_cv_.wait(lk, [&] { return done_ == n_ - 1; });
+        if (first_) std::rethrow_exception(first_);
+    }
+
+  private:
+    void call(const std::function<void(size_t)>& fn, size_t k) {
+        try {
+            fn(k);
+        } catch (...) {
+            std::lock_guard<std::mutex> lk(m_);
+            if (!first_) first_ = std::current_exception();
+        }
+    }
+    size_t n_;
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(size_t)>* task_ = nullptr;
+    uint64_t gen_ = 0;
+    size_t done_ = 0;
+    bool stop_ = false;
+    std::exception_ptr first_;
+};
 
 Runtime::Runtime(int device) { devs_.push_back(std::make_unique<DeviceRuntime>(device)); }
 
@@ -75,33 +150,20 @@ Runtime::Runtime(const std::vector<int>& devices) {
         for (size_t j = 0; j < i; ++j)
             if (devices[i] == devices[j]) throw Error(DSD_ERR_RUNTIME, "device listed twice");
     for (int d : devices) devs_.push_back(std::make_unique<DeviceRuntime>(d));
+    if (devs_.size() > 1) pool_ = std::make_unique<DevicePool>(devs_.size());
 }
 
 Runtime::~Runtime() = default;
 
-// fn(k) for every device, concurrently (one host thread per extra device);
-// the first exception is rethrown once all have finished
+// fn(k) for every device, concurrently (the persistent pool)
 template <class F>
-static void each_device(size_t n, F&& fn) {
-    if (n == 1) {
+void Runtime::each_device(F&& fn) {
+    if (!pool_) {
         fn(size_t{0});
         return;
     }
-    std::exception_ptr first;
-    std::mutex m;
-    auto run = [&](size_t k) {
-        try {
-            fn(k);
-        } catch (...) {
-            std::lock_guard<std::mutex> g(m);
-            if (!first) first = std::current_exception();
-        }
-    };
-    std::vector<std::thread> th;
-    for (size_t k = 1; k < n; ++k) th.emplace_back(run, k);
-    run(0);
-    for (auto& t : th) t.join();
-    if (first) std::rethrow_exception(first);
+    const std::function<void(size_t)> task = fn;
+    pool_->run(task);
 }
 
 void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n, bool collect,
@@ -121,7 +183,7 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
         local_of_[k] = static_cast<uint32_t>(g.size());
         g.push_back(static_cast<uint32_t>(k));
     }
-    each_device(D, [&](size_t d) {
+    each_device([&](size_t d) {
         std::vector<dsd_replica> mine(global_of_[d].size());
         for (size_t j = 0; j < mine.size(); ++j) mine[j] = reps[global_of_[d][j]];
         devs_[d]->prepare(sc, ns, mine.data(), mine.size(), collect, feature_probe, event_log);
@@ -136,7 +198,7 @@ void Runtime::launch() {
     }
     // launch() computes the lane placement on the host while k_stage runs:
     // one host thread per device keeps the devices' launches overlapped
-    each_device(devs_.size(), [&](size_t d) { devs_[d]->launch(); });
+    each_device([&](size_t d) { devs_[d]->launch(); });
 }
 
 void Runtime::sync() {
@@ -147,7 +209,7 @@ const dsd_replica_summary* Runtime::host_summaries() {
     if (devs_.size() == 1) return devs_[0]->host_summaries();
     if (gathered_.size() != n_) {
         gathered_.resize(n_);
-        each_device(devs_.size(), [&](size_t d) {
+        each_device([&](size_t d) {
             const dsd_replica_summary* s = devs_[d]->host_summaries();
             const std::vector<uint32_t>& g = global_of_[d];
             for (size_t j = 0; j < g.size(); ++j) gathered_[g[j]] = s[j];
@@ -192,7 +254,7 @@ void Runtime::probe(double* out, size_t n) {
     }
     if (n > n_) n = n_;
     std::vector<std::vector<double>> part(devs_.size());
-    each_device(devs_.size(), [&](size_t d) {
+    each_device([&](size_t d) {
         part[d].resize(global_of_[d].size() * DSD_PROBE_FIELDS);
         devs_[d]->probe(part[d].data(), global_of_[d].size());
     });

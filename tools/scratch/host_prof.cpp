@@ -29,6 +29,9 @@ int main(int argc, char** argv) {
         std::string js, cs;
         dsd::host::assemble_summaries(parts, b.points, &js, &cs);
         auto t3 = std::chrono::steady_clock::now();
+        auto sh = dsd::shard_of_replicas(b.scenarios.data(), b.replicas.data(), b.replicas.size(), 4);
+        auto t4 = std::chrono::steady_clock::now();
+        std::printf("shard_of_replicas %.2f ms (%d)\n", std::chrono::duration<double, std::milli>(t4 - t3).count(), sh[7]);
         std::printf("plan %.2f ms  pack %.2f ms  summary %.2f ms  (%zu replicas)\n",
                     std::chrono::duration<double, std::milli>(t1 - t0).count(),
                     std::chrono::duration<double, std::milli>(t2 - t1).count(),
