@@ -109,6 +109,7 @@ private:
     std::vector<uint32_t> local_of_;
     std::vector<std::vector<uint32_t>> global_of_;
     std::vector<dsd_replica_summary> gathered_;
+    bool gathered_valid_ = false;
     size_t n_ = 0;
 };
 

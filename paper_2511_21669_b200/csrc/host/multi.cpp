@@ -169,7 +169,7 @@ void Runtime::each_device(F&& fn) {
 void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps, size_t n, bool collect,
                       bool feature_probe, bool event_log) {
     n_ = n;
-    gathered_.clear();
+    gathered_valid_ = false;
     if (devs_.size() == 1) {
         devs_[0]->prepare(sc, ns, reps, n, collect, feature_probe, event_log);
         return;
@@ -191,7 +191,7 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
 }
 
 void Runtime::launch() {
-    gathered_.clear();
+    gathered_valid_ = false;
     if (devs_.size() == 1) {
         devs_[0]->launch();
         return;
@@ -207,13 +207,14 @@ void Runtime::sync() {
 
 const dsd_replica_summary* Runtime::host_summaries() {
     if (devs_.size() == 1) return devs_[0]->host_summaries();
-    if (gathered_.size() != n_) {
-        gathered_.resize(n_);
+    if (!gathered_valid_) {
+        if (gathered_.size() != n_) gathered_.resize(n_);  // (kept across batches: no re-zeroing)
         each_device([&](size_t d) {
             const dsd_replica_summary* s = devs_[d]->host_summaries();
             const std::vector<uint32_t>& g = global_of_[d];
             for (size_t j = 0; j < g.size(); ++j) gathered_[g[j]] = s[j];
         });
+        gathered_valid_ = true;
     }
     return gathered_.data();
 }
