@@ -43,9 +43,15 @@ def _count(pool):
     return sum(g["count"] for g in pool) if isinstance(pool, list) else pool
 
 
+# DSD_FUZZ_BIG=1: larger topologies and workloads (a longer campaign);
+# DSD_FUZZ_SEED: offset of the case seeds
+BIG = os.environ.get("DSD_FUZZ_BIG") == "1"
+SEED0 = int(os.environ.get("DSD_FUZZ_SEED", "0"))
+
+
 def random_config(rng, awc_model=None):
-    targets = _pool(rng, 1, 3)
-    drafts = _pool(rng, 0, 6)
+    targets = _pool(rng, 1, 8 if BIG else 3)
+    drafts = _pool(rng, 0, 40 if BIG else 6)
     rtt = rng.choice([0, 1, 4, 10, 30])
     net = {"rtt_ms": rtt, "jitter_ms": round(rng.random() * rtt, 2) if rng.random() < 0.5 else 0}
     if isinstance(targets, list) and isinstance(drafts, list) and rng.random() < 0.6:
@@ -76,7 +82,7 @@ def random_config(rng, awc_model=None):
         pol["draft_max_batch"] = rng.randint(1, 4)
     if rng.random() < 0.2:
         pol["queue_capacity"] = rng.choice([4, 16, 64])
-    wl = {"mode": "poisson", "rate_rps": rng.choice([0.5, 2, 8, 30]), "n_requests": rng.randint(1, 40),
+    wl = {"mode": "poisson", "rate_rps": rng.choice([0.5, 2, 8, 30]), "n_requests": rng.randint(1, 250 if BIG else 40),
           "acceptance_rate": round(rng.random(), 2)}
     if rng.random() < 0.25:
         wl["preset"] = rng.choice(["gsm8k-like", "cnndm-like", "humaneval-like"])
@@ -96,7 +102,7 @@ def random_config(rng, awc_model=None):
 
 @pytest.mark.parametrize("case", range(int(os.environ.get("DSD_FUZZ_CASES", "48"))))
 def test_random_config_bit_exact(sim, gen_dir, case):
-    rng = random.Random(1000 + case)
+    rng = random.Random(1000 + SEED0 + case)
     text = random_config(rng, awc_model=os.path.join(gen_dir, "model.json"))
     try:
         rep, ev, end, agg = ref.run_config(text, gen_dir, None)
@@ -116,7 +122,7 @@ def test_random_config_bit_exact(sim, gen_dir, case):
 def test_random_sweep_summary_matches_reference(sim, gen_dir, case, tmp_path):
     """Batched: a random base config swept over two axes x repetitions (many
     replicas per warp, lane placement, specialised kernel when eligible)."""
-    rng = random.Random(2000 + case)
+    rng = random.Random(2000 + SEED0 + case)
     base = random_config(rng, awc_model=os.path.join(gen_dir, "model.json"))
     (tmp_path / "base.yaml").write_text(base)
     axes = rng.sample([("network.rtt_ms", [1, 10, 40]), ("workload.acceptance_rate", [0.3, 0.7, 0.95]),
