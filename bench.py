@@ -223,6 +223,10 @@ def cpu_reference(name, threads=None, sample_points=None):
         r = reforacle.sweep_bench(text, base, threads, sample_points)
         ev, rep, sec = r["events"], r["replicas"], r["seconds"]
         k = "reference"
+        # the sim-only split: run_simulation alone vs resolve_config
+        # (+ generate_synthetic), thread-summed
+        split = {"run_simulation_share": r["sim_thread_s"] / max(r["sim_thread_s"] + r["resolve_thread_s"], 1e-12),
+                 "sim_only_events_per_sec": ev / max(r["sim_thread_s"] / threads, 1e-12)}
     else:
         import ctypes
         import restate
@@ -240,9 +244,12 @@ def cpu_reference(name, threads=None, sample_points=None):
         sec = time.perf_counter() - t
         ev, rep, k = float(sum(o.events_processed for o in out)), float(nrep), "port"
     what = "the whole sweep" if not sample_points else f"{len(sample_points)} points of the sweep"
-    return {"events": ev, "replicas": rep, "seconds": sec, "kind": k, "cores": threads,
-            "sample": f"{desc}: {what} ({int(rep)} replicas, {int(ev)} events) on {threads} threads "
-                      f"({cpu_model()})"}
+    res = {"events": ev, "replicas": rep, "seconds": sec, "kind": k, "cores": threads,
+           "sample": f"{desc}: {what} ({int(rep)} replicas, {int(ev)} events) on {threads} threads "
+                     f"({cpu_model()})"}
+    if k == "reference":
+        res["split"] = split
+    return res
 
 
 def main_reference(args, rank, world):
@@ -273,6 +280,8 @@ def main_reference(args, rank, world):
                          "sample": last["sample"]},
         "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if "split" in last:
+        line["cpu_baseline"]["split"] = last["split"]
     emit(line)
 
 
@@ -495,6 +504,8 @@ def main_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = {"value": cb["events"] / cb["seconds"], "unit": "events/s", "cores": cb["cores"],
                                 "kind": cb["kind"], "sample": cb["sample"],
                                 "replicas_per_sec": cb["replicas"] / cb["seconds"]}
+        if "split" in cb:
+            line["cpu_baseline"]["split"] = cb["split"]
     emit(line)
     if dist:
         dist.destroy_process_group()

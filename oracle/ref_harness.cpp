@@ -277,7 +277,8 @@ static int sweep_worker_run(const char* sweep_yaml, const char* base_dir, int th
 // RunResult::events_processed).  Runs the listed point indices (all when
 // n_points == 0) on `threads` std::threads with an atomic job counter, each
 // job = one point with all its repetitions, exactly as the reference worker.
-// out = {events, replicas, wall_seconds, failed_points}.
+// out = {events, replicas, wall_seconds, failed_points, run_simulation seconds,
+// resolve_config (+ generate_synthetic) seconds}, the last two summed over threads.
 int ref_sweep_bench(const char* sweep_yaml, const char* base_dir, int threads,
                     const std::int64_t* points, std::int64_t n_points, double* out, char* err,
                     std::size_t errlen) {
@@ -290,7 +291,7 @@ int ref_sweep_bench(const char* sweep_yaml, const char* base_dir, int threads,
 // RunAggregates, runner.hpp:53-60).  A failed point's rows are all -1.
 int ref_sweep_replicas(const char* sweep_yaml, const char* base_dir, int threads, double* rows, char* err,
                        std::size_t errlen) {
-    double out[4];
+    double out[6];
     return sweep_worker_run(sweep_yaml, base_dir, threads, nullptr, 0, out, rows, err, errlen);
 }
 
@@ -330,6 +331,7 @@ static int sweep_worker_run(const char* sweep_yaml, const char* base_dir, int th
         std::atomic<std::size_t> next{0};
         std::atomic<std::uint64_t> events{0};
         std::atomic<std::int64_t> replicas{0}, failed{0};
+        std::atomic<std::uint64_t> resolve_ns{0}, sim_ns{0};  // thread-summed: the sim-only split
         auto worker = [&]() {
             for (;;) {
                 std::size_t j = next.fetch_add(1);
@@ -347,8 +349,15 @@ static int sweep_worker_run(const char* sweep_yaml, const char* base_dir, int th
                     double thr = 0.0, ttft = 0.0, tpot = 0.0;
                     for (int rep = 0; rep < spec.repetitions; ++rep) {
                         std::uint64_t seed = sweep_point_seed(spec.base_seed, pid, rep);
+                        const auto ta = std::chrono::steady_clock::now();
                         ResolvedConfig rc = resolve_config(config, true, seed, spec.base_dir);
+                        const auto tb = std::chrono::steady_clock::now();
                         SimulationOutput o = run_simulation(rc);
+                        const auto tc = std::chrono::steady_clock::now();
+                        resolve_ns.fetch_add(static_cast<std::uint64_t>(
+                            std::chrono::duration_cast<std::chrono::nanoseconds>(tb - ta).count()));
+                        sim_ns.fetch_add(static_cast<std::uint64_t>(
+                            std::chrono::duration_cast<std::chrono::nanoseconds>(tc - tb).count()));
                         RunAggregates agg = aggregate_run(o.result);
                         thr += agg.throughput_rps;
                         ttft += agg.mean_ttft_ms;
@@ -391,6 +400,8 @@ static int sweep_worker_run(const char* sweep_yaml, const char* base_dir, int th
         out[1] = static_cast<double>(replicas.load());
         out[2] = secs;
         out[3] = static_cast<double>(failed.load());
+        out[4] = 1e-9 * static_cast<double>(sim_ns.load());
+        out[5] = 1e-9 * static_cast<double>(resolve_ns.load());
     });
 }
 

@@ -156,7 +156,7 @@ def sweep_replicas(sweep_yaml, base_dir, threads, n_replicas):
 
 def sweep_bench(sweep_yaml, base_dir, threads, points=None):
     c = ctypes
-    out = (c.c_double * 4)()
+    out = (c.c_double * 6)()
     err = c.create_string_buffer(4096)
     if points:
         arr = (c.c_int64 * len(points))(*points)
@@ -165,7 +165,8 @@ def sweep_bench(sweep_yaml, base_dir, threads, points=None):
         rc = lib().ref_sweep_bench(sweep_yaml.encode(), base_dir.encode(), threads, None, 0, out, err, 4096)
     if rc != 0:
         raise RefError(rc, err.value.decode())
-    return {"events": out[0], "replicas": out[1], "seconds": out[2], "failed": out[3]}
+    return {"events": out[0], "replicas": out[1], "seconds": out[2], "failed": out[3], "sim_thread_s": out[4],
+            "resolve_thread_s": out[5]}
 
 
 def gen_trace(rate, n, alpha, preset=None, prompt_median=60.0, prompt_sigma=0.4, output_median=90.0,
