@@ -175,7 +175,7 @@ constexpr int kAwcH = 64, kAwcI = 5;
 // FeatureNormalizer::transform (mlp.cpp:163-170): raw features -> model input
 DSD_HD void awc_normalize(const DevScenario& S, const double raw[5], double x[5]) {
     for (int f = 0; f < 5; ++f) {
-        double v = S.awc_log[f] ? log1p(raw[f]) : raw[f];
+        double v = S.awc_log[f] ? DSD_LOG1P(raw[f]) : raw[f];
         double span = S.awc_hi[f] - S.awc_lo[f];
         x[f] = span > 0.0 ? (v - S.awc_lo[f]) / span : 0.0;
     }

@@ -1,4 +1,4 @@
-// glibc_math.cuh — glibc 2.39's exp(), log() and cos() restated for the
+// glibc_math.cuh — glibc 2.39's exp(), log(), cos() and log1p() restated for the
 // device, so the workload generator (proj/src/sim/rng.cpp:63-77: exponential
 // gaps, Box-Muller lognormal lengths) and the AWC SiLU
 // (proj/src/awc/kernels_scalar.cpp:65-70) round exactly as the reference does
@@ -265,6 +265,90 @@ DSD_GLIBC_FN double cos(double x) {
         return (m & 2) ? -r : r;
     }
     return x - x;  // (|x| >= 105414350: outside the generator's domain; not restated)
+}
+
+// s_log1p.c (fdlibm's log1p, glibc 2.39 sysdeps/ieee754/dbl-64), as the
+// x86-64 ifunc's -mfma variant evaluates it (read off its disassembly): GCC
+// fuses R1 = z*Lp1 into the first add of R's sum (fma(z, Lp1, z2*R2)), the
+// three pair terms and the k*ln2 terms; s*(hfsq + R) is computed once for
+// both return paths and stays a plain product.  Used by the AWC feature
+// normaliser (proj/src/awc/mlp.cpp:166); the arguments are finite features.
+namespace log1p_c {
+DSD_GLIBC_CONST double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10,
+                       Lp1 = 6.666666666666735130e-01, Lp2 = 3.999999999940941908e-01,
+                       Lp3 = 2.857142874366239149e-01, Lp4 = 2.222219843214978396e-01,
+                       Lp5 = 1.818357216161805012e-01, Lp6 = 1.531383769920937332e-01,
+                       Lp7 = 1.479819860511658591e-01;
+}  // namespace log1p_c
+
+DSD_GLIBC_FN double log1p(double x) {
+    using namespace log1p_c;
+    const int32_t hx = static_cast<int32_t>(as_u64(x) >> 32);
+    const int32_t ax = hx & 0x7fffffff;
+    int32_t k = 1, hu = 0;
+    double f = 0.0, c = 0.0;
+    if (hx < 0x3FDA827A) {                                // x < 0.41422
+        if (ax >= 0x3ff00000) {                           // x <= -1
+            if (x == -1.0) return -1.80143985094819840000e+16 / 0.0;
+            return (x - x) / (x - x);
+        }
+        if (ax < 0x3e200000) {                            // |x| < 2^-29
+            if (ax < 0x3c900000) return x;                // |x| < 2^-54
+            return fma_(-(x * x), 0.5, x);                // x - x*x*0.5
+        }
+        if (hx > 0 || hx <= static_cast<int32_t>(0xbfd2bec4)) {  // -0.2929 < x < 0.41422
+            k = 0;
+            f = x;
+            hu = 1;
+        }
+    } else if (hx >= 0x7ff00000) {
+        return x + x;
+    }
+    if (k != 0) {
+        double u;
+        if (hx < 0x43400000) {
+            u = 1.0 + x;
+            hu = static_cast<int32_t>(as_u64(u) >> 32);
+            k = (hu >> 20) - 1023;
+            c = (k > 0) ? 1.0 - (u - x) : x - (u - 1.0);  // correction term
+            c /= u;
+        } else {
+            u = x;
+            hu = static_cast<int32_t>(as_u64(u) >> 32);
+            k = (hu >> 20) - 1023;
+            c = 0.0;
+        }
+        hu &= 0x000fffff;
+        const uint64_t lo = as_u64(u) & 0xffffffffull;
+        if (hu < 0x6a09e) {
+            u = as_double((static_cast<uint64_t>(static_cast<uint32_t>(hu | 0x3ff00000)) << 32) | lo);  // u
+        } else {
+            k += 1;
+            u = as_double((static_cast<uint64_t>(static_cast<uint32_t>(hu | 0x3fe00000)) << 32) | lo);  // u/2
+            hu = (0x00100000 - hu) >> 2;
+        }
+        f = u - 1.0;
+    }
+    const double hfsq = (0.5 * f) * f;
+    const double dk = static_cast<double>(k);
+    if (hu == 0) {  // |f| < 2^-20
+        if (f == 0.0) {
+            if (k == 0) return 0.0;
+            c = fma_(dk, ln2_lo, c);
+            return fma_(dk, ln2_hi, c);
+        }
+        const double R = hfsq * fma_(-0.66666666666666666, f, 1.0);
+        if (k == 0) return f - R;
+        return fma_(dk, ln2_hi, -((R - fma_(dk, ln2_lo, c)) - f));
+    }
+    const double s = f / (2.0 + f);
+    const double z = s * s;
+    const double z2 = z * z, z4 = z2 * z2, z6 = z4 * z2;
+    const double R2 = fma_(z, Lp3, Lp2), R3 = fma_(z, Lp5, Lp4), R4 = fma_(z, Lp7, Lp6);
+    const double R = fma_(z6, R4, fma_(z4, R3, fma_(z, Lp1, z2 * R2)));
+    const double P = s * (hfsq + R);
+    if (k == 0) return f - (hfsq - P);
+    return fma_(dk, ln2_hi, -((hfsq - (P + fma_(dk, ln2_lo, c))) - f));
 }
 
 }  // namespace glibc

@@ -17,16 +17,19 @@
 
 #include "glibc_math.cuh"
 
-// exp / log / cos as the reference's x86-64 glibc computes them: glibc's
-// own algorithms on the device (glibc_math.cuh), the host's libm on the host
+// exp / log / cos / log1p as the reference's x86-64 glibc computes them:
+// glibc's own algorithms on the device (glibc_math.cuh), the host's libm on
+// the host
 #ifdef __CUDA_ARCH__
 #define DSD_EXP(x) ::dsd::glibc::exp(x)
 #define DSD_LOG(x) ::dsd::glibc::log(x)
 #define DSD_COS(x) ::dsd::glibc::cos(x)
+#define DSD_LOG1P(x) ::dsd::glibc::log1p(x)
 #else
 #define DSD_EXP(x) std::exp(x)
 #define DSD_LOG(x) std::log(x)
 #define DSD_COS(x) std::cos(x)
+#define DSD_LOG1P(x) std::log1p(x)
 #endif
 
 namespace dsd {

@@ -11,6 +11,9 @@
 //   fn 1  cos(2 * pi * u)            Box-Muller angle
 //   fn 2  exp(mu + sigma * z)        lognormal lengths, mu = log(median)
 //         for medians 1..4096 and sigma 0.05..1, z from the same Box-Muller
+//   fn 3  log1p(v)                   the AWC feature normaliser
+//         (proj/src/awc/mlp.cpp:166): non-negative features up to 5000, and
+//         2^-30..2^20 scales
 // libm_check() returns the number of bitwise mismatches and how many of them
 // change llround(y) (fn 2: the request length) or llround(-m * y * 1000)
 // (fn 0: a 1-ms-mean gap in us) - the integers the engine consumes.
@@ -55,11 +58,14 @@ __global__ void k_eval(int fn, const double* x, double* y, int64_t n) {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const double v = x[i];
-        y[i] = fn == 0 ? dsd::glibc::log(v) : fn == 1 ? dsd::glibc::cos(v) : dsd::glibc::exp(v);
+        y[i] = fn == 0 ? dsd::glibc::log(v) : fn == 1 ? dsd::glibc::cos(v) : fn == 2 ? dsd::glibc::exp(v)
+                                                                                 : dsd::glibc::log1p(v);
     }
 }
 
-double host_f(int fn, double v) { return fn == 0 ? std::log(v) : fn == 1 ? std::cos(v) : std::exp(v); }
+double host_f(int fn, double v) {
+    return fn == 0 ? std::log(v) : fn == 1 ? std::cos(v) : fn == 2 ? std::exp(v) : std::log1p(v);
+}
 
 // the argument stream of fn for chunk c
 void make_inputs(int fn, uint64_t seed, int64_t c, double* x, int64_t n) {
@@ -69,6 +75,9 @@ void make_inputs(int fn, uint64_t seed, int64_t c, double* x, int64_t n) {
             x[i] = 1.0 - g.unit();
         } else if (fn == 1) {
             x[i] = 2.0 * 3.14159265358979323846 * g.unit();
+        } else if (fn == 3) {
+            const double u = g.unit();
+            x[i] = i % 3 == 0 ? u * 64.0 : i % 3 == 1 ? u * 5000.0 : std::ldexp(u, static_cast<int>(g.next() % 51) - 30);
         } else {
             const double median = 1.0 + static_cast<double>(g.next() % 4096);
             const double sigma = 0.05 + 0.95 * g.unit();

@@ -19,7 +19,8 @@ LIB = os.path.join(HERE, "native", "_build", "liblibm_check.so")
 N = int(os.environ.get("DSD_LIBM_N", str(10 ** 8)))
 
 
-@pytest.mark.parametrize("fn,name", [(0, "log(1-u)"), (1, "cos(2*pi*u)"), (2, "exp(mu+sigma*z)")])
+@pytest.mark.parametrize("fn,name", [(0, "log(1-u)"), (1, "cos(2*pi*u)"), (2, "exp(mu+sigma*z)"),
+                                     (3, "log1p(feature)")])
 def test_device_libm_matches_glibc(fn, name):
     L = ctypes.CDLL(LIB)
     mm, flips, ex = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
