@@ -532,7 +532,9 @@ void DeviceRuntime::transfer_bytes(int64_t* h2d, int64_t* d2h) const {
 // 0.5) alone, a warp of 1 / 2 / 4 / 8 / 16 lanes takes 1 / 1.68 / 2.54 /
 // 3.54 / 4.57 x the time of a lone lane (kWarpSlow).  Replicas are sorted by
 // an estimate of their cost - N x (150 + median output / E[tokens per round])
-// for a synthetic workload with a static window, E = (1 - a^(g+1)) / (1 - a):
+// in the specialised kernel (9 in the generic one, where every iteration's
+// events are general steps too) for a synthetic workload with a static
+// window, E = (1 - a^(g+1)) / (1 - a):
 // a request's general event handling (~60 steps, ~13 us on a lone lane)
 // against one session iteration (~66 ns) per round, fitted to lone-lane
 // kernel times of C5's (gamma, alpha) corners (the earlier
@@ -546,7 +548,7 @@ void DeviceRuntime::transfer_bytes(int64_t* h2d, int64_t* d2h) const {
 // nothing when the batch has no estimate or needs more than one wave.
 // Placement only chooses which thread runs which replica: results are
 // unchanged.
-static std::vector<int32_t> placement_list(const Packed& P, size_t n, int64_t warp_cap) {
+static std::vector<int32_t> placement_list(const Packed& P, size_t n, int64_t warp_cap, bool spec) {
     if (n < 2) return {};
     // a batch that nearly fills the wave densely is issue-bound, not
     // critical-path-bound: thin warps would only cost SIMT efficiency
@@ -554,7 +556,12 @@ static std::vector<int32_t> placement_list(const Packed& P, size_t n, int64_t wa
     static const double max_fill = std::getenv("DSD_PLACE_MAX_FILL") ? std::atof(std::getenv("DSD_PLACE_MAX_FILL")) : 0.75;
     if (static_cast<double>(n) > max_fill * static_cast<double>(warp_cap * kLanes)) return {};
     std::vector<double> est(P.scen.size(), 0.0);
-    static const double cost_req = std::getenv("DSD_COST_REQ") ? std::atof(std::getenv("DSD_COST_REQ")) : 150.0;
+    // the specialised kernel runs a request's iterations in its session loop,
+    // so the request's general steps weigh 150 iterations; the generic kernel
+    // handles every iteration's events as general steps too: 9 (C2's
+    // 16,384-replica sweep: 514 ms at 9, 572 ms at 150)
+    static const char* env_cost = std::getenv("DSD_COST_REQ");
+    const double cost_req = env_cost ? std::atof(env_cost) : (spec ? 150.0 : 9.0);
     for (size_t k = 0; k < P.scen.size(); ++k) {
         const DevScenario& d = P.scen[k];
         if (d.workload != 0 || d.n_drafts < 1 || d.fused_everything || d.window_kind != 0) return {};
@@ -843,7 +850,7 @@ static void place_lanes(RuntimeImpl& R) {
     int64_t warp_cap = R.sms * per_sm * (kBlock / kLanes);
     if (R.W.c.awc && (R.W.c.ns <= kSmemServers && R.smem_heap > 0 ? R.awc_warps_smem : R.awc_warps_hbm) > 0)
         warp_cap = R.sms * (R.W.c.ns <= kSmemServers && R.smem_heap > 0 ? R.awc_warps_smem : R.awc_warps_hbm);
-    std::vector<int32_t> pl = placement_list(R.packed, n, warp_cap);
+    std::vector<int32_t> pl = placement_list(R.packed, n, warp_cap, spec_launch);
     if (!pl.empty() && R.placement && R.lanes_per_warp == kLanes) {
         R.place.ensure(4 * pl.size());
         DSD_CUDA(cudaMemcpyAsync(R.place.p, pl.data(), 4 * pl.size(), cudaMemcpyHostToDevice, R.stream));
