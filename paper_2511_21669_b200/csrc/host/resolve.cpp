@@ -15,6 +15,8 @@
 #include <sys/stat.h>
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstring>
 #include <fstream>
 #include <set>
 #include <initializer_list>
@@ -557,12 +559,33 @@ Resolved resolve_config(const Node& config, bool strict, std::optional<uint64_t>
                         if (!allowed.count(f.first))
                             config_error("unknown key '" + f.first + "' in latency_profile.synth");
             }
-            const double td = s.double_or("target_decode_ms", 20.0), cr = s.double_or("cost_ratio", 0.1),
-                         bc = s.double_or("batch_coef", 0.05), cc = s.double_or("context_coef", 0.3),
-                         pp = s.double_or("prefill_ms_per_token", 0.2);
-            const std::string key = "synth:" + cfg::fmt_exact(td) + "," + cfg::fmt_exact(cr) + "," +
-                                    cfg::fmt_exact(bc) + "," + cfg::fmt_exact(cc) + "," + cfg::fmt_exact(pp);
-            rc.profile = cached(caches, &Caches::profiles, key, [&] { return synth_profile(td, cr, bc, cc, pp); });
+            const double v[5] = {s.double_or("target_decode_ms", 20.0), s.double_or("cost_ratio", 0.1),
+                                 s.double_or("batch_coef", 0.05), s.double_or("context_coef", 0.3),
+                                 s.double_or("prefill_ms_per_token", 0.2)};
+            // keyed by the five values' bit patterns (a sweep's points mostly
+            // share one synth spec: the planner thread's last lookup is
+            // reused without the cache lock)
+            thread_local uint64_t last_bits[5];
+            thread_local const Caches* last_caches = nullptr;
+            thread_local std::shared_ptr<const ProfileTable> last_profile;
+            uint64_t b[5];
+            std::memcpy(b, v, sizeof(b));
+            if (caches && last_caches == caches && last_profile && std::memcmp(b, last_bits, sizeof(b)) == 0) {
+                rc.profile = last_profile;
+            } else {
+                char key[96];
+                std::snprintf(key, sizeof(key), "synth:%016llx%016llx%016llx%016llx%016llx",
+                              static_cast<unsigned long long>(b[0]), static_cast<unsigned long long>(b[1]),
+                              static_cast<unsigned long long>(b[2]), static_cast<unsigned long long>(b[3]),
+                              static_cast<unsigned long long>(b[4]));
+                rc.profile = cached(caches, &Caches::profiles, key,
+                                    [&] { return synth_profile(v[0], v[1], v[2], v[3], v[4]); });
+                if (caches) {
+                    std::memcpy(last_bits, b, sizeof(b));
+                    last_caches = caches;
+                    last_profile = rc.profile;
+                }
+            }
         } else {
             config_error("latency_profile must be a path or {synth: {...}}");
         }

@@ -5,6 +5,8 @@
 #include "sweep.hpp"
 
 #include <algorithm>
+#include <charconv>
+#include <numeric>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -68,10 +70,21 @@ uint64_t sweep_point_seed(uint64_t base_seed, const std::string& point_id, int r
 static void point_seeds(uint64_t base_seed, const std::string& point_id, int reps, std::vector<uint64_t>& out) {
     out.resize(static_cast<size_t>(reps));
     const uint64_t h = cfg::fnv1a64(point_id, base_seed ^ 0x9e3779b97f4a7c15ULL);
-    for (int r = 0; r < reps; ++r)
-        out[static_cast<size_t>(r)] = (r == 0 && point_id == "base")
-                                          ? base_seed
-                                          : cfg::fnv1a64("#rep=" + std::to_string(r), h);
+    for (int r = 0; r < reps; ++r) {
+        if (r == 0 && point_id == "base") {
+            out[0] = base_seed;
+            continue;
+        }
+        // fnv1a64("#rep=" + to_string(r), h) without building the string
+        char buf[32] = {'#', 'r', 'e', 'p', '='};
+        const auto end = std::to_chars(buf + 5, buf + sizeof(buf), r).ptr;
+        uint64_t x = h;
+        for (const char* c = buf; c < end; ++c) {
+            x ^= static_cast<unsigned char>(*c);
+            x *= 0x100000001b3ULL;
+        }
+        out[static_cast<size_t>(r)] = x;
+    }
 }
 
 namespace {
@@ -237,6 +250,21 @@ static void plan_points(SweepBatch& b, size_t lo, size_t hi, int shard, int n_sh
     std::vector<Resolved> res(n_points);
     std::vector<char> ok(n_points, 0);
     std::vector<std::vector<uint64_t>> seeds(n_points);
+    // the axis values' text, once; and the order of the point id's sorted
+    // "key=value" parts, which does not depend on the values when the keys
+    // are distinct (a key that prefixes another compares on '=' vs its next
+    // character)
+    const size_t na = spec.axes.size();
+    std::vector<std::vector<std::string>> vtext(na);
+    for (size_t a = 0; a < na; ++a)
+        for (const Node& v : spec.axes[a].second) vtext[a].push_back(v.scalar() ? v.to_string() : v.canonical());
+    std::vector<size_t> id_order(na);
+    std::iota(id_order.begin(), id_order.end(), size_t{0});
+    std::sort(id_order.begin(), id_order.end(),
+              [&](size_t x, size_t y) { return spec.axes[x].first + "=" < spec.axes[y].first + "="; });
+    bool keys_distinct = true;
+    for (size_t k = 1; k < na; ++k)
+        if (spec.axes[id_order[k]].first == spec.axes[id_order[k - 1]].first) keys_distinct = false;
     std::atomic<size_t> next{0};
     auto worker = [&](size_t, size_t) {
         for (;;) {
@@ -245,14 +273,23 @@ static void plan_points(SweepBatch& b, size_t lo, size_t hi, int shard, int n_sh
             SweepPoint& p = b.points[idx];
             size_t rem = lo + idx;
             auto& asg = p.assignment;
-            for (size_t a = spec.axes.size(); a-- > 0;) {
-                const auto& values = spec.axes[a].second;
-                const Node& v = values[rem % values.size()];
-                rem /= values.size();
-                asg.emplace_back(spec.axes[a].first, v.scalar() ? v.to_string() : v.canonical());
+            asg.resize(na);
+            for (size_t a = na; a-- > 0;) {
+                const size_t nv = spec.axes[a].second.size();
+                asg[a] = {spec.axes[a].first, vtext[a][rem % nv]};
+                rem /= nv;
             }
-            std::reverse(asg.begin(), asg.end());
-            p.point_id = point_id_of(asg);
+            if (keys_distinct && na > 0) {
+                std::string& id = p.point_id;
+                for (size_t k = 0; k < na; ++k) {
+                    if (k) id += ';';
+                    id += asg[id_order[k]].first;
+                    id += '=';
+                    id += asg[id_order[k]].second;
+                }
+            } else {
+                p.point_id = point_id_of(asg);
+            }
             point_seeds(spec.base_seed, p.point_id, spec.repetitions, seeds[idx]);
             try {
                 res[idx] = resolve_config(point_config(spec, lo + idx), true, seeds[idx][0], spec.base_dir, caches,

@@ -87,3 +87,28 @@ def test_sweep_plan_seeds_match_reference():
     pid = "network.rtt_ms=2;policies.window.gamma=1;workload.acceptance_rate=0.53000000000000003"
     assert arr[16].seed == ref.lib().ref_sweep_point_seed(42, pid.encode(), 0)
     L.dsd_sweep_plan_free(p)
+
+
+def test_sweep_point_ids_and_seeds_match_reference():
+    """Axes declared out of sorted order: every replica's seed must be the
+    reference's sweep_point_seed of the point id it builds (sorted "key=value"
+    parts joined by ';', sweep.cpp:51-73)."""
+    import itertools
+    axes = [("workload.rate_rps", [1, 2]), ("network.jitter_ms", [0, 1]), ("network.rtt_ms", [10, 20]),
+            ("policies.window.gamma", [2, 3])]
+    spec = "base: c1_single_pair.yaml\nseed: 7\nrepetitions: 3\naxes:\n" + "".join(
+        f"  {k}: [{', '.join(str(v) for v in vals)}]\n" for k, vals in axes)
+    L = _lib.lib()
+    p = ctypes.c_void_p()
+    err = ctypes.create_string_buffer(1024)
+    assert L.dsd_plan_sweep(spec.encode(), CFG.encode(), 0, 1, ctypes.byref(p), err, 1024) == 0, err.value
+    reps = ctypes.c_void_p()
+    n = L.dsd_sweep_plan_replicas(p, ctypes.byref(reps))
+    assert n == 16 * 3
+    arr = ctypes.cast(reps, ctypes.POINTER(restate.Replica))
+    # points in declaration order, last axis fastest
+    for k, combo in enumerate(itertools.product(*[vals for _, vals in axes])):
+        pid = ";".join(sorted(f"{key}={v}" for (key, _), v in zip(axes, combo)))
+        for r in range(3):
+            assert arr[k * 3 + r].seed == ref.lib().ref_sweep_point_seed(7, pid.encode(), r), (k, r, pid)
+    L.dsd_sweep_plan_free(p)
