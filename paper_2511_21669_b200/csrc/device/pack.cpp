@@ -134,8 +134,11 @@ void pack_batch_into(Packed& P, const dsd_scenario* sc, size_t ns, const dsd_rep
     Caps& c = P.caps;
     c = Caps{};
     bool any_pairs = false;
+    double last_pm_in = std::nan(""), last_pm = 0.0, last_om_in = std::nan(""), last_om = 0.0;
     std::vector<int64_t> scen_bw(ns, 0), scen_nr(ns, 0);
     std::map<const dsd_grid*, int64_t> grid_tables;
+    const dsd_grid* last_grids = nullptr;
+    auto last_git = grid_tables.end();
     for (size_t k = 0; k < ns; ++k) {
         const dsd_scenario& s = sc[k];
         DevScenario& d = ds[k];
@@ -180,7 +183,9 @@ void pack_batch_into(Packed& P, const dsd_scenario* sc, size_t ns, const dsd_rep
             // (engine.cpp:10-15); when every link is jitter-free the jitter stream
             // is never observable, so the engine skips its draws.
             const size_t ndev = s.n_drafts > 0 ? nl : 1;
-            std::vector<DevLink> dl(ndev);
+            DevLink dl_small[8];
+            std::vector<DevLink> dl_big(ndev > 8 ? ndev : 0);
+            DevLink* dl = ndev > 8 ? dl_big.data() : dl_small;
             bool jitter_free = true;
             for (size_t l = 0; l < ndev; ++l) {
                 dl[l].rtt_ms = s.links[l].rtt_ms;
@@ -188,12 +193,13 @@ void pack_batch_into(Packed& P, const dsd_scenario* sc, size_t ns, const dsd_rep
                 dl[l].fixed_us = std::llround((s.links[l].rtt_ms / 2.0 + 0.0) * 1000.0);
                 if (s.links[l].jitter_ms != 0.0) jitter_free = false;
             }
-            d.o_links = B.put(dl.data(), sizeof(DevLink) * ndev, false);
+            d.o_links = B.put(dl, sizeof(DevLink) * ndev, false);
             d.jitter_free = jitter_free ? 1 : 0;
         }
         // grids
         if (s.n_grids < 1 || !s.grids) cfg_error(where() + "latency profile has no grids");
-        auto git = grid_tables.find(s.grids);
+        // (a sweep's scenarios share one profile: the last lookup first)
+        auto git = (last_grids == s.grids) ? last_git : grid_tables.find(s.grids);
         if (git == grid_tables.end()) {
             std::vector<DevGrid> g(s.n_grids);
             for (int gi = 0; gi < s.n_grids; ++gi) {
@@ -219,6 +225,8 @@ void pack_batch_into(Packed& P, const dsd_scenario* sc, size_t ns, const dsd_rep
             int64_t off = B.put(g.data(), sizeof(DevGrid) * g.size(), false);
             git = grid_tables.emplace(s.grids, off).first;
         }
+        last_grids = s.grids;
+        last_git = git;
         d.o_grids = git->second;
         d.n_grids = s.n_grids;
         for (int i = 0; i < s.n_targets; ++i)
@@ -304,8 +312,17 @@ void pack_batch_into(Packed& P, const dsd_scenario* sc, size_t ns, const dsd_rep
             d.rate_rps = s.rate_rps;
             d.mean_gap_ms = 1000.0 / s.rate_rps;
             d.alpha = s.acceptance_rate;
-            d.p_mu = std::log(s.prompt_median);  // host libm, as the reference (trace.cpp:163-164)
-            d.o_mu = std::log(s.output_median);
+            // host libm, as the reference (trace.cpp:163-164); repeated medians reuse the last log
+            if (s.prompt_median != last_pm_in || std::signbit(s.prompt_median) != std::signbit(last_pm_in)) {
+                last_pm_in = s.prompt_median;
+                last_pm = std::log(s.prompt_median);
+            }
+            if (s.output_median != last_om_in || std::signbit(s.output_median) != std::signbit(last_om_in)) {
+                last_om_in = s.output_median;
+                last_om = std::log(s.output_median);
+            }
+            d.p_mu = last_pm;
+            d.o_mu = last_om;
             d.p_sigma = s.prompt_sigma;
             d.o_sigma = s.output_sigma;
             d.p_cap = s.prompt_cap;
