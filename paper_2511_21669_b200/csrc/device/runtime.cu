@@ -906,9 +906,11 @@ static SoloCfg solo_cfg(const RuntimeImpl& R) {
         std::min<int64_t>(R.smem_optin, R.smem_per_sm / per_sm) - 1024;  // (static shared memory: the step stats)
     int64_t fixed = (c.awc ? ((static_cast<int64_t>(sizeof(AwcWarpScratch)) + 15) & ~int64_t(15)) : 0) +
                     ((static_cast<int64_t>(kServerFields) * c.ns * 4 + 15) & ~int64_t(15));
-    // heap: 1,024 slots or 2 per server (C4-static/-AWC single runs peak below
-    // 1,024; an overflow costs an HBM re-run, not a wrong result)
-    const int64_t hmin = std::min<int64_t>(R.solo_heap > 0 ? R.solo_heap : c.hc, std::max<int64_t>(1024, 2 * c.ns));
+    // heap: 1,024 slots or 1 per server (C4-static/-AWC single runs peak below
+    // 1,024; an overflow costs an HBM re-run, not a wrong result; a larger
+    // heap takes L1 from the records: C4-AWC 7.10 s at 1,024 slots, 7.45 s
+    // at 2,080)
+    const int64_t hmin = std::min<int64_t>(R.solo_heap > 0 ? R.solo_heap : c.hc, std::max<int64_t>(1024, c.ns));
     if (fixed + 16 * hmin > budget) return s;
     // AWC: the staged weights when they fit too (every decision reads all of them)
     if (R.W.awc_stage_off >= 0 && fixed + static_cast<int64_t>(R.awc_wbytes) + 16 * hmin <= budget) {
