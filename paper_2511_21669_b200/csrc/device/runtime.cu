@@ -132,6 +132,9 @@ __device__ __forceinline__ uint32_t vote_kind(unsigned best) {
 // kAwc kernels run with blocks of up to kAwcMaxThreads threads: one block
 // per SM shares one shared-memory copy of the WC-DNN weights (staging).
 constexpr int kAwcMaxThreads = 512;
+// event-heap slots of the specialised kernel's overflow re-run (45.6 KB per
+// block of two warps: few replicas, so occupancy does not matter there)
+constexpr int kSpecRerunHeap = 32;
 template <bool kSmem, bool kStats, bool kSpec = false, bool kAwc = false, int kSpecLimit = kSpecStack>
 __global__ void __launch_bounds__(kAwc ? kAwcMaxThreads : kBlock,
                                   kAwc ? 1 : (kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_BLOCKS))
@@ -436,6 +439,7 @@ struct RuntimeImpl {
     int solo_heap = 0;     // DSD_SOLO_HEAP: cap on its heap slots (tests: force the HBM re-run)
     bool solo_rec = true;  // DSD_SOLO_REC=0: keep the records in HBM
     bool smem_launch = false;
+    bool spec_rerun = false;  // the last launch re-ran overflows in the specialised kernel first
     void* pinned = nullptr;  // host_summaries() buffer (page-locked)
     bool pinned_valid = false;  // it holds the last launch's summaries
     bool retried = false;       // sync() ran retry_heap_overflows for the last launch
@@ -1106,12 +1110,29 @@ void DeviceRuntime::launch() {
         ++R.launches;
     }
     if (smem) {
-        // replicas whose event heap outgrew shared memory run again from HBM
-        R.ovf.ensure(4 * (R.n + 1));
+        // replicas whose event heap outgrew shared memory (or the specialised
+        // kernel's action stack) run again: a specialised batch first in the
+        // same kernel with a kSpecRerunHeap-slot heap (a lone C5 replica takes
+        // ~2 ms there and ~30 ms in the HBM variant), then whatever still fails
+        // from HBM
+        R.ovf.ensure(8 * (R.n + 1));
         int32_t* count = static_cast<int32_t*>(R.ovf.p);
         int32_t* list = count + 1;
-        DSD_CUDA(cudaMemsetAsync(count, 0, 4, R.stream));
         const unsigned g2 = static_cast<unsigned>((R.n + 255) / 256);
+        const bool spec = !solo.on && R.spec_ok && R.specialize && !R.collect && !R.W.probe;
+        R.spec_rerun = spec;
+        if (spec) {
+            int32_t* count1 = count + R.n + 1;
+            int32_t* list1 = count1 + 1;
+            DSD_CUDA(cudaMemsetAsync(count1, 0, 4, R.stream));
+            k_collect_overflow<<<g2, 256, 0, R.stream>>>(R.W, list1, count1);
+            k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, nullptr, list1, count1);
+            const size_t rbytes = (kBlock / kLanes) * smem_warp_bytes(2, kSpecRerunHeap, false);
+            k_simulate<true, false, true><<<grid, kBlock, rbytes, R.stream>>>(R.W, list1, count1, kSpecRerunHeap);
+            DSD_CUDA(cudaGetLastError());
+            R.launches += 3;
+        }
+        DSD_CUDA(cudaMemsetAsync(count, 0, 4, R.stream));
         k_collect_overflow<<<g2, 256, 0, R.stream>>>(R.W, list, count);
         k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, R.collect ? static_cast<int64_t*>(R.ltot.p) : nullptr, list,
                                                 count);
@@ -1190,9 +1211,14 @@ void DeviceRuntime::sync() {
         retry_heap_overflows(R);
         R.retried = true;
     }
-    if (R.ran && R.n > 0 && R.smem_launch && std::getenv("DSD_HOST_TIMING")) {  // replicas the shared-memory kernel handed to the HBM variant
-        int32_t rerun = 0;
+    if (R.ran && R.n > 0 && R.smem_launch && std::getenv("DSD_HOST_TIMING")) {  // replicas the shared-memory kernel handed on
+        int32_t rerun = 0, rerun1 = 0;
         DSD_CUDA(cudaMemcpy(&rerun, R.ovf.p, sizeof(rerun), cudaMemcpyDeviceToHost));
+        if (R.spec_rerun) {
+            DSD_CUDA(cudaMemcpy(&rerun1, static_cast<int32_t*>(R.ovf.p) + R.n + 1, sizeof(rerun1), cudaMemcpyDeviceToHost));
+            std::fprintf(stderr, "[dsd sync] re-run in the specialised kernel (%d-slot heap): %d of %zu replicas\n",
+                         kSpecRerunHeap, rerun1, R.n);
+        }
         std::fprintf(stderr, "[dsd sync] re-run on the HBM variant: %d of %zu replicas\n", rerun, R.n);
     }
     if (R.step_stats && R.W.step_stats) {

@@ -166,9 +166,10 @@ def test_large_sweep_parallel_aggregation_matches_reference():
 
 def test_specialized_stack_overflow_reruns_on_hbm_variant(capfd):
     """The specialised kernel keeps a shorter action stack; a replica that
-    overflows it fails with kFailStack and runs again on the HBM variant.
-    DSD_SPEC_STACK_LIMIT=1 forces that for nearly every replica: the summaries
-    must not change."""
+    overflows it fails with kFailStack and runs again - in the specialised
+    kernel with the full stack and a larger heap, then (if it still fails) on
+    the HBM variant.  DSD_SPEC_STACK_LIMIT=1 forces that for nearly every
+    replica: the summaries must not change."""
     from paper_2511_21669_b200 import Simulator
     spec = ("base: c1_single_pair.yaml\nseed: 5\nrepetitions: 3\naxes:\n"
             "  policies.window.gamma: [1, 4, 9, 16]\n  network.rtt_ms: [2, 30]\n"
@@ -181,7 +182,7 @@ def test_specialized_stack_overflow_reruns_on_hbm_variant(capfd):
     finally:
         del os.environ["DSD_SPEC_STACK_LIMIT"], os.environ["DSD_HOST_TIMING"]
     err = capfd.readouterr().err
-    m = re.search(r"re-run on the HBM variant: (\d+) of (\d+) replicas", err)
+    m = re.search(r"re-run in the specialised kernel \(\d+-slot heap\): (\d+) of (\d+) replicas", err)
     assert m and int(m.group(1)) > int(m.group(2)) // 2, err[-2000:]
     assert out.summary_json == js
     assert out.summary_csv == cs
