@@ -135,6 +135,9 @@ constexpr int kAwcMaxThreads = 512;
 // event-heap slots of the specialised kernel's overflow re-run (45.6 KB per
 // block of two warps: few replicas, so occupancy does not matter there)
 constexpr int kSpecRerunHeap = 32;
+// the generic shared-memory kernel's (up to 4 servers and their session slots:
+// <= 50 KB per block)
+constexpr int kGenRerunHeap = 16;
 template <bool kSmem, bool kStats, bool kSpec = false, bool kAwc = false, int kSpecLimit = kSpecStack>
 __global__ void __launch_bounds__(kAwc ? kAwcMaxThreads : kBlock,
                                   kAwc ? 1 : (kSpec ? DSD_SPEC_MIN_BLOCKS : DSD_MIN_BLOCKS))
@@ -439,7 +442,8 @@ struct RuntimeImpl {
     int solo_heap = 0;     // DSD_SOLO_HEAP: cap on its heap slots (tests: force the HBM re-run)
     bool solo_rec = true;  // DSD_SOLO_REC=0: keep the records in HBM
     bool smem_launch = false;
-    bool spec_rerun = false;  // the last launch re-ran overflows in the specialised kernel first
+    bool spec_rerun = false;  // the last launch re-ran overflows in its shared-memory kernel first
+    int rerun_heap = 0;       // ... with this many heap slots
     void* pinned = nullptr;  // host_summaries() buffer (page-locked)
     bool pinned_valid = false;  // it holds the last launch's summaries
     bool retried = false;       // sync() ran retry_heap_overflows for the last launch
@@ -1120,15 +1124,27 @@ void DeviceRuntime::launch() {
         int32_t* list = count + 1;
         const unsigned g2 = static_cast<unsigned>((R.n + 255) / 256);
         const bool spec = !solo.on && R.spec_ok && R.specialize && !R.collect && !R.W.probe;
-        R.spec_rerun = spec;
-        if (spec) {
+        // (the generic shared-memory kernel likewise, with a kGenRerunHeap-slot heap; not AWC)
+        const bool gen = !solo.on && !spec && !R.W.c.awc;
+        R.spec_rerun = spec || gen;
+        R.rerun_heap = spec ? kSpecRerunHeap : kGenRerunHeap;
+        if (spec || gen) {
             int32_t* count1 = count + R.n + 1;
             int32_t* list1 = count1 + 1;
             DSD_CUDA(cudaMemsetAsync(count1, 0, 4, R.stream));
             k_collect_overflow<<<g2, 256, 0, R.stream>>>(R.W, list1, count1);
             k_stage<<<grid, kBlock, 0, R.stream>>>(R.W, nullptr, list1, count1);
-            const size_t rbytes = (kBlock / kLanes) * smem_warp_bytes(2, kSpecRerunHeap, false);
-            k_simulate<true, false, true><<<grid, kBlock, rbytes, R.stream>>>(R.W, list1, count1, kSpecRerunHeap);
+            if (spec) {
+                const size_t rbytes = (kBlock / kLanes) * smem_warp_bytes(2, kSpecRerunHeap, false);
+                k_simulate<true, false, true><<<grid, kBlock, rbytes, R.stream>>>(R.W, list1, count1, kSpecRerunHeap);
+            } else {
+                const size_t rbytes = (kBlock / kLanes) * smem_warp_bytes(R.W.c.ns, kGenRerunHeap, false);
+                cudaFuncAttributes fa;
+                DSD_CUDA(cudaFuncGetAttributes(&fa, k_simulate<true, false>));
+                DSD_CUDA(cudaFuncSetAttribute(k_simulate<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              R.smem_optin - static_cast<int>(fa.sharedSizeBytes)));
+                k_simulate<true, false><<<grid, kBlock, rbytes, R.stream>>>(R.W, list1, count1, kGenRerunHeap);
+            }
             DSD_CUDA(cudaGetLastError());
             R.launches += 3;
         }
@@ -1216,8 +1232,8 @@ void DeviceRuntime::sync() {
         DSD_CUDA(cudaMemcpy(&rerun, R.ovf.p, sizeof(rerun), cudaMemcpyDeviceToHost));
         if (R.spec_rerun) {
             DSD_CUDA(cudaMemcpy(&rerun1, static_cast<int32_t*>(R.ovf.p) + R.n + 1, sizeof(rerun1), cudaMemcpyDeviceToHost));
-            std::fprintf(stderr, "[dsd sync] re-run in the specialised kernel (%d-slot heap): %d of %zu replicas\n",
-                         kSpecRerunHeap, rerun1, R.n);
+            std::fprintf(stderr, "[dsd sync] re-run in the shared-memory kernel (%d-slot heap): %d of %zu replicas\n",
+                         R.rerun_heap, rerun1, R.n);
         }
         std::fprintf(stderr, "[dsd sync] re-run on the HBM variant: %d of %zu replicas\n", rerun, R.n);
     }

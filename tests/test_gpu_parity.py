@@ -182,7 +182,7 @@ def test_specialized_stack_overflow_reruns_on_hbm_variant(capfd):
     finally:
         del os.environ["DSD_SPEC_STACK_LIMIT"], os.environ["DSD_HOST_TIMING"]
     err = capfd.readouterr().err
-    m = re.search(r"re-run in the specialised kernel \(\d+-slot heap\): (\d+) of (\d+) replicas", err)
+    m = re.search(r"re-run in the shared-memory kernel \(\d+-slot heap\): (\d+) of (\d+) replicas", err)
     assert m and int(m.group(1)) > int(m.group(2)) // 2, err[-2000:]
     assert out.summary_json == js
     assert out.summary_csv == cs
