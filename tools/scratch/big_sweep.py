@@ -1,5 +1,7 @@
-"""The C5 sweep at 4x the repetitions (262,144 replicas, ~3.5e9 events) on one
-GPU: summary JSON/CSV against the reference's run_sweep, and the timing."""
+"""The C5 sweep at more repetitions (default 64: 262,144 replicas, ~3.5e9
+events) on one or more GPUs of one handle: summary JSON/CSV against the
+reference's run_sweep, and the timing.
+  python tools/scratch/big_sweep.py [repetitions] [devices]"""
 import os
 import sys
 import time
@@ -10,8 +12,9 @@ import reforacle as ref  # noqa: E402
 from paper_2511_21669_b200 import Simulator  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+ndev = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 spec = open("configs/c5_sweep_65536.yaml").read().replace("repetitions: 16", f"repetitions: {reps}")
-with Simulator(0) as s:
+with Simulator(list(range(ndev)) if ndev > 1 else 0) as s:
     t = time.perf_counter()
     out = s.run_sweep(spec, base_dir="configs")
     dt = time.perf_counter() - t
