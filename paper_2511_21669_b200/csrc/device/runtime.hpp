@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "dsdsim.h"
+#include "../host/uninit.hpp"
 
 namespace dsd {
 
@@ -108,7 +109,8 @@ private:
     std::vector<int32_t> dev_of_;
     std::vector<uint32_t> local_of_;
     std::vector<std::vector<uint32_t>> global_of_;
-    std::vector<dsd_replica_summary> gathered_;
+    std::vector<std::vector<dsd_replica>> mine_;  // each device's replicas (storage kept across batches)
+    host::uvector<dsd_replica_summary> gathered_;  // (no zero fill: every element is written)
     bool gathered_valid_ = false;
     size_t n_ = 0;
 };

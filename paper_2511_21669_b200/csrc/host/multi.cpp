@@ -44,32 +44,75 @@ std::vector<int32_t> shard_of_replicas(const dsd_scenario* sc, const dsd_replica
     if (n_shards <= 1 || n == 0) return shard;
     // cost per distinct scenario; replicas by decreasing cost = the
     // scenarios sorted by cost, then a counting sort of the replicas by their
-    // scenario's rank (replica order within a rank)
+    // scenario's rank (replica order within a rank).  One pass over the
+    // replicas gathers the scenario count, the per-scenario replica counts
+    // and whether each scenario's replicas are contiguous (memory-bound at a
+    // million replicas: every pass over them costs ~3 ms)
     uint32_t ns = 0;
-    for (size_t k = 0; k < n; ++k) ns = std::max(ns, reps[k].scenario + 1);
+    std::vector<size_t> cnt;
+    bool grouped = true;
+    for (size_t k = 0; k < n; ++k) {
+        const uint32_t t = reps[k].scenario;
+        if (t >= ns) {
+            ns = t + 1;
+            cnt.resize(ns, 0);
+        }
+        ++cnt[t];
+        grouped = grouped && (k == 0 || t >= reps[k - 1].scenario);
+    }
     std::vector<double> sc_cost(ns, 0.0);
-    std::vector<char> used(ns, 0);
-    for (size_t k = 0; k < n; ++k) used[reps[k].scenario] = 1;
     for (uint32_t s = 0; s < ns; ++s)
-        if (used[s]) sc_cost[s] = replica_cost_estimate(sc[s]);
+        if (cnt[s]) sc_cost[s] = replica_cost_estimate(sc[s]);
     std::vector<uint32_t> sorder(ns), srank(ns);
     std::iota(sorder.begin(), sorder.end(), 0u);
     std::stable_sort(sorder.begin(), sorder.end(), [&](uint32_t a, uint32_t b) { return sc_cost[a] > sc_cost[b]; });
+    // the deal position of the i-th replica in cost order: 0..N-1, N-1..0, ...
+    const int32_t N = n_shards;
+    auto snake = [N](size_t i, int32_t& pos, int32_t& dir) {
+        const size_t round = i / static_cast<size_t>(N);
+        const int32_t p = static_cast<int32_t>(i % static_cast<size_t>(N));
+        dir = round % 2 == 0 ? 1 : -1;
+        pos = dir > 0 ? p : N - 1 - p;
+    };
+    auto step = [N](int32_t& pos, int32_t& dir) {
+        pos += dir;
+        if (pos == N || pos < 0) {
+            dir = -dir;
+            pos += dir;
+        }
+    };
+    // Fast path - every scenario's replicas contiguous and in scenario order,
+    // as plan_sweep lays them out: each scenario's run is dealt from its
+    // offset in cost order with sequential writes (a million-replica batch:
+    // ~19 -> ~2 ms)
+    if (grouped) {
+        std::vector<size_t> first(static_cast<size_t>(ns) + 1, 0);  // replicas of scenario s: [first[s], first[s+1])
+        for (uint32_t t = 0; t < ns; ++t) first[t + 1] = first[t] + cnt[t];
+        size_t base = 0;
+        for (uint32_t i = 0; i < ns; ++i) {
+            const uint32_t sc_i = sorder[i];
+            const size_t lo = first[sc_i], hi = first[sc_i + 1];
+            if (lo == hi) continue;
+            int32_t pos, dir;
+            snake(base, pos, dir);
+            for (size_t k = lo; k < hi; ++k) {
+                shard[k] = pos;
+                step(pos, dir);
+            }
+            base += hi - lo;
+        }
+        return shard;
+    }
     for (uint32_t i = 0; i < ns; ++i) srank[sorder[i]] = i;
     std::vector<size_t> start(static_cast<size_t>(ns) + 1, 0);
     for (size_t k = 0; k < n; ++k) ++start[srank[reps[k].scenario] + 1];
     for (uint32_t i = 0; i < ns; ++i) start[i + 1] += start[i];
     std::vector<uint32_t> order(n);
     for (size_t k = 0; k < n; ++k) order[start[srank[reps[k].scenario]]++] = static_cast<uint32_t>(k);
-    // dealt 0..N-1, N-1..0, 0..N-1, ... (counters: no 64-bit division per replica)
     int32_t pos = 0, dir = 1;
     for (size_t i = 0; i < n; ++i) {
         shard[order[i]] = pos;
-        pos += dir;
-        if (pos == n_shards || pos < 0) {
-            dir = -dir;
-            pos += dir;
-        }
+        step(pos, dir);
     }
     return shard;
 }
@@ -151,6 +194,7 @@ Runtime::Runtime(const std::vector<int>& devices) {
             if (devices[i] == devices[j]) throw Error(DSD_ERR_RUNTIME, "device listed twice");
     for (int d : devices) devs_.push_back(std::make_unique<DeviceRuntime>(d));
     if (devs_.size() > 1) pool_ = std::make_unique<DevicePool>(devs_.size());
+    mine_.resize(devs_.size());
 }
 
 Runtime::~Runtime() = default;
@@ -177,15 +221,23 @@ void Runtime::prepare(const dsd_scenario* sc, size_t ns, const dsd_replica* reps
     const size_t D = devs_.size();
     dev_of_ = shard_of_replicas(sc, reps, n, static_cast<int>(D));
     local_of_.resize(n);
-    global_of_.assign(D, {});
-    for (size_t k = 0; k < n; ++k) {
-        std::vector<uint32_t>& g = global_of_[static_cast<size_t>(dev_of_[k])];
-        local_of_[k] = static_cast<uint32_t>(g.size());
-        g.push_back(static_cast<uint32_t>(k));
-    }
+    global_of_.resize(D);
+    // every device's thread picks its replicas out of the deal (one scan of
+    // the shard ids each, in parallel; a million-replica batch took ~15 ms
+    // as one serial pass of push_backs)
     each_device([&](size_t d) {
-        std::vector<dsd_replica> mine(global_of_[d].size());
-        for (size_t j = 0; j < mine.size(); ++j) mine[j] = reps[global_of_[d][j]];
+        std::vector<uint32_t>& g = global_of_[d];
+        g.clear();
+        g.reserve(n / D + 1);
+        const int32_t di = static_cast<int32_t>(d);
+        for (size_t k = 0; k < n; ++k)
+            if (dev_of_[k] == di) {
+                local_of_[k] = static_cast<uint32_t>(g.size());
+                g.push_back(static_cast<uint32_t>(k));
+            }
+        std::vector<dsd_replica>& mine = mine_[d];
+        mine.resize(g.size());
+        for (size_t j = 0; j < mine.size(); ++j) mine[j] = reps[g[j]];
         devs_[d]->prepare(sc, ns, mine.data(), mine.size(), collect, feature_probe, event_log);
     });
 }

@@ -331,7 +331,7 @@ static void plan_points(SweepBatch& b, size_t lo, size_t hi, int shard, int n_sh
                 x.scenario = static_cast<uint32_t>(s);
                 x.seed = seeds[idx][rep];
                 x.gen_seed = r.gen_seed_fixed ? r.gen_seed : x.seed;
-                b.replica_origin[g] = {static_cast<int64_t>(idx), static_cast<int>(rep)};
+                b.replica_origin[g] = {static_cast<int64_t>(idx), static_cast<int32_t>(rep)};
             }
         }
     });

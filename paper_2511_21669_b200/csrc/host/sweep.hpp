@@ -9,6 +9,7 @@
 
 #include "../device/runtime.hpp"
 #include "resolve.hpp"
+#include "uninit.hpp"
 #include "yaml.hpp"
 
 namespace dsd::host {
@@ -21,6 +22,11 @@ struct SweepSpec {
     std::vector<std::pair<std::string, std::vector<cfg::Node>>> axes;
     static SweepSpec from_node(const cfg::Node& node, const std::string& base_dir);
     size_t point_count() const;
+};
+
+struct ReplicaOrigin {
+    int64_t first;   // point
+    int32_t second;  // repetition
 };
 
 struct SweepPoint {
@@ -43,8 +49,8 @@ struct SweepBatch {
     std::vector<Resolved> resolved;          // one per resolvable point
     std::vector<int64_t> point_scenario;     // point -> index in resolved, -1 when failed
     std::vector<dsd_scenario> scenarios;
-    std::vector<dsd_replica> replicas;
-    std::vector<std::pair<int64_t, int>> replica_origin;  // replica -> (point, rep)
+    uvector<dsd_replica> replicas;
+    uvector<ReplicaOrigin> replica_origin;  // replica -> (point, rep)
     size_t point_base = 0;  // points[i] is sweep point point_base + i
 };
 
