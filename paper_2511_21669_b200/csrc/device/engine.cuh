@@ -442,11 +442,11 @@ enum : uint32_t {
      (1u << kActNetResult) | (1u << kActBeginAwc) | (1u << kActNone))
 #endif
 constexpr uint32_t kBarrierKinds = DSD_BARRIER_KINDS;
-// The generic shared-memory kernel (up to 4 servers; solo mode): the session
-// entry and the AWC continuation only.  Its lanes' chains are short and cheap
-// with the state in shared memory; measured (B200) against the general set:
-// a 8,192-replica dynamic-window sweep 57.1 -> 54.8 ms, the 768-replica AWC
-// sweep 157 -> 153 ms; the HBM variant keeps the general set (the C2 sweep
+// The generic shared-memory kernel (up to 4 servers; solo mode) and every AWC
+// kernel: the session entry and the AWC continuation only.  Measured (B200)
+// against the general set: a 8,192-replica dynamic-window sweep 57.1 -> 54.8
+// ms, the 768-replica AWC sweep 157 -> 153 ms, 4,096 C3 replicas (HBM, AWC)
+// 3.51 -> 2.87 s; the non-AWC HBM variant keeps the general set (the C2 sweep
 // 512 -> 677 ms with this one).
 #ifndef DSD_SMEM_BARRIER_KINDS
 #define DSD_SMEM_BARRIER_KINDS ((1u << kActBegin) | (1u << kActBeginAwc) | (1u << kActNone))

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kAwc ? kAwcMaxThreads : kBlock,
     }
     if constexpr (kAwc) awc->req[threadIdx.x % kLanes] = 0;
     Engine e(W, W.scen[W.rep_scen[r]], r, sbase, hb, kb, hcap, nsc, hot, kSpec, awc, kSpecLimit, lstride, srec);
-    e.smem_barriers = kSmem && !kSpec;
+    e.smem_barriers = (kSmem || kAwc) && !kSpec;
     if (live) e.init();
     uint32_t kind = live ? e.next_kind() : static_cast<uint32_t>(kActNone);
     // kStats: per-step-kind cycle profile (DSD_STEP_STATS=1), one block-level
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kAwc ? kAwcMaxThreads : kBlock,
                     e.step();
                 }
                 kind = e.next_kind_unchecked();
-            } while (!(((kSpec ? kSpecBarrierKinds : kSmem ? kSmemBarrierKinds : kBarrierKinds) >> kind) & 1u));
+            } while (!(((kSpec ? kSpecBarrierKinds : (kSmem || kAwc) ? kSmemBarrierKinds : kBarrierKinds) >> kind) & 1u));
             // (a failed replica stops at its next pop: next_kind_unchecked)
         }
         if constexpr (kStats) ++iters;
